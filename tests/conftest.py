@@ -1,0 +1,53 @@
+"""Shared pytest wiring: the `gpu` marker and golden-fixture loaders."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built libkst_b200.so")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"), allow_pickle=False)
+
+
+def basis_of(d, key):
+    return None if bool(d[key + "_none"]) else d[key]
+
+
+def cfg_of(d):
+    import ast
+    return ast.literal_eval(str(d["cfg"]))
+
+
+def scene_cube(d, store_key="cube"):
+    """Cube of a pipeline golden case: stored, or regenerated and hash-checked."""
+    import hashlib
+    from paper_1604_03622_b200 import scenes
+    if store_key in d.files:
+        return np.array(d[store_key])
+    cfg = scenes.SceneConfig(**cfg_of(d))
+    hist = scenes.gen_clutter(cfg)
+    for b, f, a in d["targets"]:
+        hist = scenes.inject_target(hist, int(b), float(f), complex(a))
+    cube = hist.data[0]
+    assert hashlib.sha256(np.ascontiguousarray(cube).tobytes()).hexdigest() == str(d["cube_sha"])
+    return cube
+
+
+PIPELINE_CASES = ["readme_q16"] + [f"sweep_q64_ra{a}_rb{b}" for a in (1, 2, 3) for b in (1, 2, 3)] + [
+    "classical_q64", "droptemporal_q64", "cfg1_q256"]
+
+
+def map_tolerance(ref, m0, rel=1e-4, floor=1e-5):
+    """SURVEY.md §8c map rule: |v - v_ref| <= rel*|v_ref| + floor*M0."""
+    return rel * np.abs(ref) + floor * m0

@@ -1,0 +1,154 @@
+/*
+ * kst_b200.h -- C ABI of libkst_b200.so, the B200 (sm_100a) Kron-STAP hot path.
+ *
+ * The reference (`kronstap`, pure Python, /root/reference/pkg/src/kronstap,
+ * abbreviated src/) has no FFI: its boundary is the Python functions
+ * re-exported by src/__init__.py:17-45. Each entry point below replaces one
+ * of those functions; the citation on each names the reference interface.
+ * INTEGRATION.md shows the ctypes binding a kronstap maintainer would add.
+ *
+ * Conventions
+ *  - Complex data are interleaved (re, im) float64 pairs, i.e. numpy
+ *    complex128 memory; row-major (C order) like numpy.
+ *  - "dev" pointers are CUDA device pointers; "host" pointers are host
+ *    memory. Every call is ordered on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream). Calls that must report a
+ *    data-dependent outcome (iteration counts, degenerate input, non-finite
+ *    data) synchronise that stream before returning.
+ *  - Return value: KST_OK or one of the KST_ERR_* codes, which the Python
+ *    layer maps onto the reference's exception classes (src/errors.py:9-30).
+ *    No C++ exception crosses this boundary. kst_last_error() gives text.
+ *  - One kst_ctx per (device, host thread). The context owns a grow-only
+ *    device workspace; callers own every input/output buffer.
+ *  - Results are deterministic: fixed-order reductions, no float atomics.
+ */
+#ifndef KST_B200_H
+#define KST_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define KST_OK 0
+#define KST_ERR_DIMENSION 1  /* -> DimensionError       */
+#define KST_ERR_DATA 2       /* -> DataError            */
+#define KST_ERR_DEGENERATE 3 /* -> DegenerateInputError */
+#define KST_ERR_CUDA 100     /* CUDA runtime / launch failure */
+#define KST_ERR_NOCONV 101   /* internal eigensolver failed to converge */
+
+#define KST_KIND_KRON 0
+#define KST_KIND_CLASSICAL 1
+
+typedef struct kst_ctx kst_ctx;
+
+/* Context lifetime. */
+int kst_ctx_create(int device, kst_ctx** out);
+int kst_ctx_destroy(kst_ctx* ctx);
+const char* kst_last_error(const kst_ctx* ctx);
+int kst_version(void);
+
+/*
+ * Sample covariance -- replaces `sample_covariance(snapshots, p, q)`
+ * (src/lrkron.py:53-78): S = (1/n) X^T conj(X), exactly Hermitian.
+ *   X  dev, (n, d) complex, d = p*q snapshot rows (src/layout.py:35-41)
+ *   S  dev, (d, d) complex, written in full (both triangles)
+ */
+int kst_scm(kst_ctx* ctx, const double* X, int64_t n, int64_t d, double* S,
+            void* stream);
+
+/*
+ * LR-Kron estimate -- replaces `lr_kron_estimate(scm, rank_spatial,
+ * rank_temporal, tol, max_iter, keep_iterates)` (src/lrkron.py:118-230).
+ *   S            dev (pq, pq) complex
+ *   validate     1: run the reference's input checks (src/lrkron.py:100-115)
+ *   spatial      dev (p, p) complex   <- KronCovEstimate.spatial
+ *   temporal     dev (q, q) complex   <- KronCovEstimate.temporal (may be NULL)
+ *   tb_vectors   dev (q, rank_temporal) complex, tb_values host (rank_temporal):
+ *                top eigenpairs of the final b with the reference's order and
+ *                phase conventions (src/linalg.py:82-121); NULL to skip. Only
+ *                filled when rank_temporal < q.
+ *   residuals    host (max_iter) float64; *n_residuals entries written
+ *   iter_spatial dev (max_iter, p, p), iter_b dev (max_iter, q, q): per-
+ *                iteration (spatial, b) copies for keep_iterates; may be NULL
+ */
+int kst_lrkron(kst_ctx* ctx, const double* S, int p, int q, int rank_spatial,
+               int rank_temporal, double tol, int max_iter, int validate,
+               double* spatial, double* temporal, double* tb_vectors,
+               double* tb_values, double* residuals, int* n_residuals,
+               int* iterations, int* converged, double* iter_spatial,
+               double* iter_b, void* stream);
+
+/*
+ * Hermitian eigen-helpers with the reference's conventions.
+ * kst_heig_top: top `r` eigenpairs (descending; ties by dominant index;
+ *   pivot entry real positive) of a dev (n, n) Hermitian matrix ->
+ *   values host (r), vectors dev (n, r). Replaces hermitian_eig
+ *   (src/linalg.py:82-121) restricted to the leading r pairs.
+ * kst_eig_truncate: replaces eig_truncate (src/linalg.py:124-144).
+ * kst_subspace_basis: replaces subspace_basis (src/filters.py:58-73);
+ *   *keep = number of columns written (0 means the reference's None).
+ */
+int kst_heig_top(kst_ctx* ctx, const double* M, int n, int r, double* values,
+                 double* vectors, void* stream);
+int kst_eig_truncate(kst_ctx* ctx, const double* M, int n, int rank,
+                     double* out, void* stream);
+int kst_subspace_basis(kst_ctx* ctx, const double* M, int n, int rank,
+                       double tol, double* basis, int* keep, void* stream);
+
+/*
+ * Detection image -- replaces `detection_image(filt, cube, dopplers,
+ * spatial_grid)` (src/filters.py:243-275) for the projection filters
+ * (`StapFilter.apply_matrix`, src/filters.py:88-116, kinds kron/classical),
+ * and `pass_images` (src/multipass.py:83-102) when groups > 1.
+ *   cube      dev (n, p, q) complex
+ *   ua        dev (p, ka) complex or NULL (ka = 0)  -- spatial_basis
+ *   ub        dev (q, kb) complex or NULL (kb = 0)  -- temporal_basis
+ *   dopplers  host (D) float64 (any values; d/D grids take the folded-DFT path)
+ *   grid      host (G, p) complex spatial candidates; rows split into
+ *             `groups` equal consecutive blocks, one map per block
+ *   values    dev (groups, n, D) float64
+ */
+int kst_detect(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
+               const double* ua, int ka, const double* ub, int kb, int kind,
+               int spatial_only, const double* dopplers, int D,
+               const double* grid, int G, int groups, double* values,
+               void* stream);
+
+/*
+ * Whole-cube clutter filter -- replaces StapFilter.apply_matrix
+ * (src/filters.py:88-116) applied bin by bin, as `kronstap filter` does
+ * (src/cli.py:177-206). cube/out dev (n, p, q) complex.
+ */
+int kst_filter(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
+               const double* ua, int ka, const double* ub, int kb, int kind,
+               int spatial_only, double* out, void* stream);
+
+/* change_detect (src/multipass.py:105-123): out = |a - b| (or a - b). */
+int kst_change(kst_ctx* ctx, const double* a, const double* b, int64_t count,
+               int is_signed, double* out, void* stream);
+
+/*
+ * Fused frame pipeline -- the README library sequence (pkg/README.md:144-161):
+ * sample_covariance -> lr_kron_estimate -> build_filter(kind) ->
+ * detection_image, on one cube, without materialising host copies.
+ *   cube dev (n, p, q); values dev (groups, n, D); summary host (8 doubles):
+ *   [iterations, converged, ka, kb, last residual, 0, 0, 0]
+ */
+int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
+                 int rank_spatial, int rank_temporal, double tol, int max_iter,
+                 int kind, const double* dopplers, int D, const double* grid,
+                 int G, int groups, double* values, double* summary,
+                 void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* KST_B200_H */

@@ -1,0 +1,209 @@
+// C ABI of libkst_b200.so (declared in include/kst_b200.h): context,
+// workspace and the extern "C" entry points. No C++ exception crosses it.
+#include <cstdarg>
+#include <cstring>
+
+#include "common.cuh"
+
+int set_err(kst_ctx* ctx, int code, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return code;
+}
+
+void* ws_get(kst_ctx* ctx, int slot, size_t bytes) {
+  auto& s = ctx->slots[slot];
+  if (bytes == 0) bytes = 1;
+  if (s.bytes >= bytes) return s.ptr;
+  if (s.ptr) {
+    // in-flight kernels may still read the old buffer
+    cudaDeviceSynchronize();
+    cudaFree(s.ptr);
+    s.ptr = nullptr;
+    s.bytes = 0;
+  }
+  size_t want = bytes + bytes / 8 + 256;
+  if (cudaMalloc(&s.ptr, want) != cudaSuccess) {
+    cudaGetLastError();
+    s.ptr = nullptr;
+    return nullptr;
+  }
+  s.bytes = want;
+  return s.ptr;
+}
+
+void* pinned_get(kst_ctx* ctx, size_t bytes) {
+  if (ctx->pinned_bytes >= bytes) return ctx->pinned;
+  if (ctx->pinned) {
+    cudaDeviceSynchronize();
+    cudaFreeHost(ctx->pinned);
+  }
+  size_t want = std::max<size_t>(bytes, 1 << 16);
+  if (cudaMallocHost(&ctx->pinned, want) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->pinned = nullptr;
+    ctx->pinned_bytes = 0;
+    return nullptr;
+  }
+  ctx->pinned_bytes = want;
+  return ctx->pinned;
+}
+
+namespace {
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+#define CTX_GUARD(ctx)                          \
+  if (!(ctx)) return KST_ERR_DIMENSION;         \
+  DeviceGuard guard__((ctx)->device);           \
+  (ctx)->err.clear();
+
+extern "C" {
+
+int kst_version(void) { return 1; }
+
+int kst_ctx_create(int device, kst_ctx** out) {
+  if (!out) return KST_ERR_DIMENSION;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+    cudaGetLastError();
+    return KST_ERR_CUDA;
+  }
+  kst_ctx* c = new (std::nothrow) kst_ctx();
+  if (!c) return KST_ERR_CUDA;
+  c->device = device;
+  DeviceGuard g(device);
+  cudaFree(nullptr);  // establish the primary context
+  *out = c;
+  return KST_OK;
+}
+
+int kst_ctx_destroy(kst_ctx* ctx) {
+  if (!ctx) return KST_OK;
+  {
+    DeviceGuard g(ctx->device);
+    cudaDeviceSynchronize();
+    for (auto& s : ctx->slots)
+      if (s.ptr) cudaFree(s.ptr);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  }
+  delete ctx;
+  return KST_OK;
+}
+
+const char* kst_last_error(const kst_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int kst_scm(kst_ctx* ctx, const double* X, int64_t n, int64_t d, double* S, void* stream) {
+  CTX_GUARD(ctx);
+  return kst::scm(ctx, (const cplx*)X, n, d, (cplx*)S, (cudaStream_t)stream);
+}
+
+int kst_lrkron(kst_ctx* ctx, const double* S, int p, int q, int rank_spatial, int rank_temporal,
+               double tol, int max_iter, int validate, double* spatial, double* temporal,
+               double* tb_vectors, double* tb_values, double* residuals, int* n_residuals,
+               int* iterations, int* converged, double* iter_spatial, double* iter_b,
+               void* stream) {
+  CTX_GUARD(ctx);
+  kst::FitOut fit;
+  int rc = kst::lrkron(ctx, (const cplx*)S, p, q, rank_spatial, rank_temporal, tol, max_iter,
+                       validate, (cplx*)spatial, (cplx*)temporal, (cplx*)tb_vectors, tb_values,
+                       &fit, (cplx*)iter_spatial, (cplx*)iter_b, (cudaStream_t)stream);
+  if (iterations) *iterations = fit.iterations;
+  if (converged) *converged = fit.converged;
+  if (n_residuals) *n_residuals = fit.n_res;
+  if (residuals)
+    for (int k = 0; k < fit.n_res; ++k) residuals[k] = fit.residuals[k];
+  return rc;
+}
+
+int kst_heig_top(kst_ctx* ctx, const double* M, int n, int r, double* values, double* vectors,
+                 void* stream) {
+  CTX_GUARD(ctx);
+  KST_TRY(kst::herm_check(ctx, (const cplx*)M, n, (cudaStream_t)stream));
+  return kst::heig_top(ctx, (const cplx*)M, n, r, values, (cplx*)vectors, (cudaStream_t)stream);
+}
+
+int kst_eig_truncate(kst_ctx* ctx, const double* M, int n, int rank, double* out, void* stream) {
+  CTX_GUARD(ctx);
+  return kst::eig_truncate(ctx, (const cplx*)M, n, rank, (cplx*)out, (cudaStream_t)stream);
+}
+
+int kst_subspace_basis(kst_ctx* ctx, const double* M, int n, int rank, double tol, double* basis,
+                       int* keep, void* stream) {
+  CTX_GUARD(ctx);
+  return kst::subspace_basis(ctx, (const cplx*)M, n, rank, tol, (cplx*)basis, keep,
+                             (cudaStream_t)stream);
+}
+
+int kst_detect(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, const double* ua, int ka,
+               const double* ub, int kb, int kind, int spatial_only, const double* dopplers, int D,
+               const double* grid, int G, int groups, double* values, void* stream) {
+  CTX_GUARD(ctx);
+  return kst::detect(ctx, (const cplx*)cube, n, p, q, (const cplx*)ua, ka, (const cplx*)ub, kb, kind,
+                     spatial_only, dopplers, D, (const cplx*)grid, G, groups, values,
+                     (cudaStream_t)stream);
+}
+
+int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int rank_spatial,
+                 int rank_temporal, double tol, int max_iter, int kind, const double* dopplers,
+                 int D, const double* grid, int G, int groups, double* values, double* summary,
+                 void* stream) {
+  CTX_GUARD(ctx);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t d = (int64_t)p * q;
+  if (n < 1 || p < 1 || q < 1) return set_err(ctx, KST_ERR_DIMENSION, "pipeline: empty cube");
+  cplx* S = (cplx*)ws_get(ctx, WS_S, sizeof(cplx) * d * d);
+  cplx* spatial = (cplx*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 2 + 64);
+  if (!S || !spatial) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+  cplx* ua = spatial + p * p;
+  KST_TRY(kst::scm(ctx, (const cplx*)cube, n, d, S, st));
+  // the temporal basis must survive until detection: dedicated slot
+  const bool full_b = rank_temporal == q;
+  cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal + 64);
+  cplx* temporal = full_b ? (cplx*)ws_get(ctx, WS_PIPE_T, sizeof(cplx) * (size_t)q * q) : nullptr;
+  if (!ub || (full_b && !temporal)) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+  std::vector<double> tbv(rank_temporal > 0 ? rank_temporal : 1);
+  kst::FitOut fit;
+  KST_TRY(kst::lrkron(ctx, S, p, q, rank_spatial, rank_temporal, tol, max_iter, 0, spatial,
+                      temporal, full_b ? nullptr : ub, full_b ? nullptr : tbv.data(), &fit,
+                      nullptr, nullptr, st));
+  // build_filter (src/filters.py:164-175): U_A from the spatial factor
+  int ka = 0, kb = 0;
+  KST_TRY(kst::subspace_basis(ctx, spatial, p, rank_spatial, 1e-9, ua, &ka, st));
+  if (full_b) {
+    KST_TRY(kst::subspace_basis(ctx, temporal, q, rank_temporal, 1e-9, ub, &kb, st));
+  } else if (tbv[0] > 0.0) {
+    while (kb < rank_temporal && tbv[kb] > 1e-9 * tbv[0]) ++kb;
+  }
+  KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, ka ? ua : nullptr, ka, kb ? ub : nullptr, kb,
+                      kind, 0, dopplers, D, (const cplx*)grid, G, groups, values, st));
+  if (summary) {
+    summary[0] = fit.iterations;
+    summary[1] = fit.converged;
+    summary[2] = ka;
+    summary[3] = kb;
+    summary[4] = fit.residuals.empty() ? 0.0 : fit.residuals.back();
+    summary[5] = summary[6] = summary[7] = 0.0;
+  }
+  return KST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// Shared device/host helpers for libkst_b200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/kst_b200.h"
+
+typedef double2 cplx;  // (re, im) == numpy complex128 memory
+
+__host__ __device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+__host__ __device__ __forceinline__ cplx cmulc(cplx a, cplx b) {
+  return cmk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__host__ __device__ __forceinline__ cplx cconj(cplx a) { return cmk(a.x, -a.y); }
+__host__ __device__ __forceinline__ cplx cscale(cplx a, double s) { return cmk(a.x * s, a.y * s); }
+// acc += a * b
+__device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += a * conj(b)
+__device__ __forceinline__ void cfmac(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.y, b.x, acc.y);
+  acc.y = fma(-a.x, b.y, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cfmca(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__host__ __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+
+constexpr int kNumSMs = 148;  // B200
+
+// ---------------------------------------------------------------- context
+struct kst_ctx {
+  int device = 0;
+  std::string err;
+  // grow-only device workspace slots (never shrink; freed at destroy)
+  struct Slot {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  Slot slots[24];
+  // pinned host staging for small device->host reads
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  void* cusolver = nullptr;  // cusolverDnHandle_t, created lazily (heig.cu fallback)
+};
+
+enum WsSlot {
+  WS_S = 0,        // pq x pq covariance (pipeline)
+  WS_B = 1,        // q x q temporal iterate
+  WS_PART = 2,     // per-CTA partial sums
+  WS_SMALL = 3,    // small matrices / scalars (spatial iterate, flags)
+  WS_EIG = 4,      // eigensolver block vectors
+  WS_EIG2 = 5,     // eigensolver scratch
+  WS_DET = 6,      // detection scratch (spectra / coefficients)
+  WS_DET2 = 7,     // detection constants (twiddles, grids, bases spectra)
+  WS_PREP = 8,     // Gram operand planes
+  WS_UB = 9,       // pipeline temporal basis
+  WS_UA = 10,      // pipeline spatial basis
+  WS_VALS = 11,    // misc
+  WS_CUSOLVER = 12, // cuSOLVER workspace (fallback path only)
+  WS_TMP = 13,      // short-lived copies
+  WS_PIPE_UB = 14,  // pipeline: temporal basis (lives until detection)
+  WS_PIPE_T = 15,   // pipeline: full temporal factor (rank_temporal == q only)
+  WS_PIPE_SP = 16   // pipeline: spatial factor + spatial basis
+};
+
+void* ws_get(kst_ctx* ctx, int slot, size_t bytes);  // may return nullptr on OOM
+void* pinned_get(kst_ctx* ctx, size_t bytes);
+
+int set_err(kst_ctx* ctx, int code, const char* fmt, ...);
+
+#define KST_CUDA(ctx, call)                                                               \
+  do {                                                                                    \
+    cudaError_t e__ = (call);                                                             \
+    if (e__ != cudaSuccess)                                                               \
+      return set_err((ctx), KST_ERR_CUDA, "%s failed: %s (%s:%d)", #call,                 \
+                     cudaGetErrorString(e__), __FILE__, __LINE__);                        \
+  } while (0)
+
+#define KST_LAUNCH(ctx)                                                                   \
+  do {                                                                                    \
+    cudaError_t e__ = cudaGetLastError();                                                 \
+    if (e__ != cudaSuccess)                                                               \
+      return set_err((ctx), KST_ERR_CUDA, "kernel launch failed: %s (%s:%d)",             \
+                     cudaGetErrorString(e__), __FILE__, __LINE__);                        \
+  } while (0)
+
+#define KST_TRY(expr)              \
+  do {                             \
+    int rc__ = (expr);             \
+    if (rc__ != KST_OK) return rc__; \
+  } while (0)
+
+static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+// ---------------------------------------------------------------- device reductions
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fixed-order block sum (deterministic): every thread gets the result.
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+    t = (l < NT / 32) ? sh[l] : 0.0;
+    t = warp_sum(t);
+    if (l == 0) sh[0] = t;
+  }
+  __syncthreads();
+  return sh[0];
+}
+
+// ---------------------------------------------------------------- internal API between units
+namespace kst {
+// gram.cu
+int scm(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, cudaStream_t st);
+// heig.cu
+struct TopEig {
+  int r = 0;
+  std::vector<double> values;  // descending, host
+  cplx* vectors = nullptr;     // dev (n, r) row-major
+};
+int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cplx* vectors,
+             cudaStream_t st);
+int small_heig(kst_ctx* ctx, const cplx* M, int n, double* values_dev, cplx* vectors_dev,
+               cudaStream_t st);
+int truncate_from_pairs(kst_ctx* ctx, const double* values_host, const cplx* vectors, int n,
+                        int r, double top_abs, cplx* out, cudaStream_t st);
+int eig_truncate(kst_ctx* ctx, const cplx* M, int n, int rank, cplx* out, cudaStream_t st);
+int subspace_basis(kst_ctx* ctx, const cplx* M, int n, int rank, double tol, cplx* basis, int* keep,
+                   cudaStream_t st);
+int herm_check(kst_ctx* ctx, const cplx* M, int n, cudaStream_t st);  // DataError if not Hermitian
+// lrkron.cu
+struct FitOut {
+  int iterations = 0, converged = 0, n_res = 0;
+  std::vector<double> residuals;
+};
+int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol, int max_iter,
+           int validate, cplx* spatial, cplx* temporal, cplx* tb_vectors, double* tb_values,
+           FitOut* fit, cplx* iter_spatial, cplx* iter_b, cudaStream_t st);
+// detect.cu
+int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
+           const cplx* ub, int kb, int kind, int spatial_only, const double* dop_host, int D,
+           const cplx* grid_host, int G, int groups, double* values, cudaStream_t st);
+}  // namespace kst

@@ -1,0 +1,511 @@
+// K5/K6: detection image for the projection filters, FP64.
+//
+// Reference (src/filters.py:243-275, 88-116): per bin m,
+//   F = filter(X_m)                       (kron: X - (X conj(U_B)) U_B^T, then
+//                                          X - U_A (U_A^H X); classical: joint)
+//   values[m, d] = max_g | sum_i conj(H[g,i]) sum_t F[i,t] conj(T[t,d]) |,
+//   T[t,d] = exp(2 pi i t f_d) / sqrt(q).
+//
+// B200 formulation: the filter is linear and acts on the
+// channel and pulse axes separately, so it commutes with the pulse-axis
+// transform. Per (bin, channel) row we
+//   1. compute the temporal coefficients c[k] = sum_t x[t] conj(U_B[t,k]),
+//   2. fold t mod D and run a length-D mixed-radix Stockham DFT in shared
+//      memory (exact integer twiddle indices into an FP64 table), which for
+//      the uniform grid f_d = d/D equals sum_t x[t] exp(-2 pi i t d / D);
+//      any other Doppler set takes a direct sum,
+// then per (bin, Doppler) subtract sum_k c[k] DFT(U_B[:,k])[d], apply the
+// spatial projector, the spatial candidates, |.|, max, and write f64.
+// Multipass (`pass_images`, src/multipass.py:83-102) filters once and
+// emits one map per row block of the stacked grid (`groups`).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int NT = 256;
+constexpr int kMaxFactors = 32;
+constexpr int kMaxP = 16;
+constexpr int kMaxKB = 64;
+
+struct Plan {
+  int D;
+  int nf;
+  int radix[kMaxFactors];
+};
+
+__constant__ Plan c_plan;
+
+// twiddle table w[k] = exp(-2 pi i k / D)
+__global__ void twiddle_kernel(cplx* w, int D) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < D; k += gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)D, &s, &c);
+    w[k] = cmk(c, s);
+  }
+}
+
+// In-place (ping-pong) Stockham DFT of length D over shared buffers.
+// Returns pointer to the buffer holding the result.
+__device__ cplx* stockham(cplx* a, cplx* b, const cplx* __restrict__ w, int D) {
+  int Ns = 1;
+  for (int f = 0; f < c_plan.nf; ++f) {
+    const int R = c_plan.radix[f];
+    const int DR = D / R;
+    const int step = D / (Ns * R);
+    for (int e = threadIdx.x; e < D; e += blockDim.x) {
+      const int j = e % DR, u = e / DR;
+      const int k = j % Ns;
+      const int base = (k + u * Ns) * step;  // exponent multiplier
+      cplx acc = cmk(0, 0);
+      int idx = 0;
+      for (int r = 0; r < R; ++r) {
+        cfma(acc, a[j + r * DR], w[idx]);
+        idx += base;
+        if (idx >= D) idx -= D * (idx / D);
+      }
+      b[(j / Ns) * Ns * R + k + u * Ns] = acc;
+    }
+    __syncthreads();
+    cplx* t = a;
+    a = b;
+    b = t;
+    Ns *= R;
+  }
+  return a;
+}
+
+// One CTA per row (bin m, channel i) of `src` (rows x q, row stride q):
+// coefficients against U_B and the folded DFT (uniform) or direct sum.
+__global__ void __launch_bounds__(NT) row_spectrum_kernel(
+    const cplx* __restrict__ src, int64_t rows, int q, const cplx* __restrict__ ub, int kb,
+    const cplx* __restrict__ w, int D, int uniform, const double* __restrict__ dop,
+    cplx* __restrict__ spec, cplx* __restrict__ coef, int* __restrict__ nonfinite) {
+  extern __shared__ __align__(16) cplx smem[];
+  __shared__ double red[32];
+  const int64_t row = blockIdx.x;
+  const cplx* x = src + row * q;
+  // 1. temporal coefficients c[k] = sum_t x[t] conj(ub[t, k])
+  int bad = 0;
+  for (int k = 0; k < kb; ++k) {
+    double cr = 0.0, ci = 0.0;
+    for (int t = threadIdx.x; t < q; t += NT) {
+      const cplx v = x[t], u = ub[(int64_t)t * kb + k];
+      cr = fma(v.x, u.x, cr);
+      cr = fma(v.y, u.y, cr);
+      ci = fma(v.y, u.x, ci);
+      ci = fma(-v.x, u.y, ci);
+    }
+    cr = block_sum<NT>(cr, red);
+    ci = block_sum<NT>(ci, red);
+    if (threadIdx.x == 0) coef[row * kb + k] = cmk(cr, ci);
+  }
+  if (uniform) {
+    cplx* a = smem;
+    cplx* b = smem + D;
+    cplx* tw = smem + 2 * D;
+    for (int k = threadIdx.x; k < D; k += NT) tw[k] = w[k];
+    // 2. fold t mod D (ascending t: deterministic)
+    for (int tp = threadIdx.x; tp < D; tp += NT) {
+      cplx acc = cmk(0, 0);
+      for (int t = tp; t < q; t += D) {
+        const cplx v = x[t];
+        if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+        acc = cadd(acc, v);
+      }
+      a[tp] = acc;
+    }
+    __syncthreads();
+    cplx* res = stockham(a, b, tw, D);
+    for (int d = threadIdx.x; d < D; d += NT) spec[row * D + d] = res[d];
+  } else {
+    // direct sum with the reference's phase: theta = 2 pi (t f_d)
+    cplx* xs = smem;
+    for (int t = threadIdx.x; t < q; t += NT) {
+      const cplx v = x[t];
+      if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+      xs[t] = v;
+    }
+    __syncthreads();
+    const double twopi = 6.283185307179586;
+    for (int d = threadIdx.x; d < D; d += NT) {
+      const double f = dop[d];
+      cplx acc = cmk(0, 0);
+      for (int t = 0; t < q; ++t) {
+        double s, c;
+        sincos(twopi * ((double)t * f), &s, &c);
+        cfmac(acc, xs[t], cmk(c, s));  // x * conj(exp(i theta))
+      }
+      spec[row * D + d] = acc;
+    }
+  }
+  if (bad) atomicOr(nonfinite, 1);
+}
+
+// Transpose U_B (q x kb) into kb rows of length q.
+__global__ void transpose_kernel(const cplx* __restrict__ ub, int q, int kb, cplx* __restrict__ out) {
+  const int64_t total = (int64_t)q * kb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e / kb), k = (int)(e % kb);
+    out[(int64_t)k * q + t] = ub[e];
+  }
+}
+
+struct CombineArgs {
+  int P, D, ka, kb, G, groups;
+  int mode;  // 0: temporal coef (kron), 1: joint coef (classical), 2: none
+  int spatial;  // apply spatial projector
+  double inv_sqrt_q;
+};
+
+// grid: (ceil(D / NT), n). One thread per Doppler.
+__global__ void __launch_bounds__(NT) combine_kernel(
+    const cplx* __restrict__ spec, const cplx* __restrict__ coef, const cplx* __restrict__ ubspec,
+    const cplx* __restrict__ ua, const cplx* __restrict__ hconj, CombineArgs a,
+    double* __restrict__ values, int64_t n) {
+  __shared__ cplx s_ua[kMaxP * kMaxP];
+  __shared__ cplx s_c[kMaxP * kMaxKB];
+  extern __shared__ __align__(16) cplx s_h[];  // G x P conj grid
+  const int64_t m = blockIdx.y;
+  const int P = a.P;
+  for (int e = threadIdx.x; e < P * a.ka; e += NT) s_ua[e] = ua[e];
+  for (int e = threadIdx.x; e < a.G * P; e += NT) s_h[e] = hconj[e];
+  if (a.mode != 2) {
+    for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = coef[m * P * a.kb + e];
+  }
+  __syncthreads();
+  if (a.mode == 1) {
+    // classical: E = U_A (U_A^H c)  (src/filters.py:115-116)
+    __shared__ cplx s_e[kMaxP * kMaxKB];
+    for (int e = threadIdx.x; e < P * a.kb; e += NT) {
+      const int i = e / a.kb, k = e % a.kb;
+      cplx acc = cmk(0, 0);
+      for (int al = 0; al < a.ka; ++al) {
+        cplx inner = cmk(0, 0);
+        for (int j = 0; j < P; ++j) cfmca(inner, s_ua[j * a.ka + al], s_c[j * a.kb + k]);
+        cfma(acc, s_ua[i * a.ka + al], inner);
+      }
+      s_e[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = s_e[e];
+    __syncthreads();
+  }
+  const int d = blockIdx.x * NT + threadIdx.x;
+  if (d >= a.D) return;
+  cplx y[kMaxP];
+#pragma unroll
+  for (int i = 0; i < kMaxP; ++i)
+    if (i < P) y[i] = spec[(m * P + i) * a.D + d];
+  if (a.mode != 2) {
+    for (int k = 0; k < a.kb; ++k) {
+      const cplx u = ubspec[(int64_t)k * a.D + d];
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) {
+          const cplx cu = cmul(s_c[i * a.kb + k], u);
+          y[i] = csub(y[i], cu);
+        }
+    }
+  }
+  if (a.spatial) {
+    for (int al = 0; al < a.ka; ++al) {
+      cplx alpha = cmk(0, 0);
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) cfmca(alpha, s_ua[i * a.ka + al], y[i]);
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) y[i] = csub(y[i], cmul(s_ua[i * a.ka + al], alpha));
+    }
+  }
+  const int per = a.G / a.groups;
+  for (int gr = 0; gr < a.groups; ++gr) {
+    double best = 0.0;
+    for (int g = gr * per; g < (gr + 1) * per; ++g) {
+      cplx z = cmk(0, 0);
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) cfma(z, s_h[g * P + i], y[i]);
+      const double mag = hypot(z.x * a.inv_sqrt_q, z.y * a.inv_sqrt_q);
+      best = (g == gr * per) ? mag : fmax(best, mag);
+    }
+    values[((int64_t)gr * n + m) * a.D + d] = best;
+  }
+}
+
+__global__ void change_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                              int64_t count, int is_signed, double* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = a[e] - b[e];
+    out[e] = is_signed ? v : fabs(v);
+  }
+}
+
+// c[row][k] = sum_t x[t] conj(U_B[t,k]); one CTA per (bin, channel) row
+__global__ void __launch_bounds__(NT) coef_kernel(const cplx* __restrict__ src, int q,
+                                                  const cplx* __restrict__ ub, int kb,
+                                                  cplx* __restrict__ coef, int* __restrict__ nonfinite) {
+  __shared__ double red[32];
+  const int64_t row = blockIdx.x;
+  const cplx* x = src + row * q;
+  int bad = 0;
+  for (int t = threadIdx.x; t < q; t += NT) {
+    const cplx v = x[t];
+    if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+  }
+  if (bad) atomicOr(nonfinite, 1);
+  for (int k = 0; k < kb; ++k) {
+    double cr = 0.0, ci = 0.0;
+    for (int t = threadIdx.x; t < q; t += NT) {
+      const cplx v = x[t], u = ub[(int64_t)t * kb + k];
+      cr = fma(v.x, u.x, cr);
+      cr = fma(v.y, u.y, cr);
+      ci = fma(v.y, u.x, ci);
+      ci = fma(-v.x, u.y, ci);
+    }
+    cr = block_sum<NT>(cr, red);
+    ci = block_sum<NT>(ci, red);
+    if (threadIdx.x == 0) coef[row * kb + k] = cmk(cr, ci);
+  }
+}
+
+// Time-domain projection filter (StapFilter.apply_matrix, src/filters.py:88-116):
+// grid (ceil(q / NT), n); one thread per pulse t of bin m.
+__global__ void __launch_bounds__(NT) filter_apply_kernel(
+    const cplx* __restrict__ cube, const cplx* __restrict__ coef, const cplx* __restrict__ ub,
+    const cplx* __restrict__ ua, int P, int q, int ka, int kb, int mode, int spatial,
+    cplx* __restrict__ out) {
+  __shared__ cplx s_ua[kMaxP * kMaxP];
+  __shared__ cplx s_c[kMaxP * kMaxKB];
+  const int64_t m = blockIdx.y;
+  for (int e = threadIdx.x; e < P * ka; e += NT) s_ua[e] = ua[e];
+  if (mode != 2)
+    for (int e = threadIdx.x; e < P * kb; e += NT) s_c[e] = coef[m * P * kb + e];
+  __syncthreads();
+  if (mode == 1) {
+    __shared__ cplx s_e[kMaxP * kMaxKB];
+    for (int e = threadIdx.x; e < P * kb; e += NT) {
+      const int i = e / kb, k = e % kb;
+      cplx acc = cmk(0, 0);
+      for (int al = 0; al < ka; ++al) {
+        cplx inner = cmk(0, 0);
+        for (int j = 0; j < P; ++j) cfmca(inner, s_ua[j * ka + al], s_c[j * kb + k]);
+        cfma(acc, s_ua[i * ka + al], inner);
+      }
+      s_e[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * kb; e += NT) s_c[e] = s_e[e];
+    __syncthreads();
+  }
+  const int t = blockIdx.x * NT + threadIdx.x;
+  if (t >= q) return;
+  cplx y[kMaxP];
+#pragma unroll
+  for (int i = 0; i < kMaxP; ++i)
+    if (i < P) y[i] = cube[(m * P + i) * q + t];
+  if (mode != 2) {
+    for (int k = 0; k < kb; ++k) {
+      const cplx u = ub[(int64_t)t * kb + k];
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) y[i] = csub(y[i], cmul(s_c[i * kb + k], u));
+    }
+  }
+  if (spatial) {
+    for (int al = 0; al < ka; ++al) {
+      cplx alpha = cmk(0, 0);
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) cfmca(alpha, s_ua[i * ka + al], y[i]);
+#pragma unroll
+      for (int i = 0; i < kMaxP; ++i)
+        if (i < P) y[i] = csub(y[i], cmul(s_ua[i * ka + al], alpha));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxP; ++i)
+    if (i < P) out[(m * P + i) * q + t] = y[i];
+}
+
+// filter semantics -> (mode, spatial) (src/filters.py:98-116)
+// mode 0: temporal projection coefficients, 1: joint (classical), 2: none
+void filter_mode(int kind, bool has_a, bool has_b, int spatial_only, int& mode, int& spatial) {
+  mode = 2;
+  spatial = 0;
+  if (kind == KST_KIND_KRON) {
+    mode = (has_b && !spatial_only) ? 0 : 2;
+    spatial = has_a ? 1 : 0;
+  } else if (has_a) {
+    if (spatial_only) spatial = 1;
+    else if (has_b) mode = 1;
+  }
+}
+
+int plan_factors(int D, Plan& p) {
+  p.D = D;
+  p.nf = 0;
+  int x = D;
+  while (x % 4 == 0) {
+    p.radix[p.nf++] = 4;
+    x /= 4;
+  }
+  while (x % 2 == 0) {
+    p.radix[p.nf++] = 2;
+    x /= 2;
+  }
+  for (int f = 3; (int64_t)f * f <= x; f += 2)
+    while (x % f == 0) {
+      p.radix[p.nf++] = f;
+      x /= f;
+    }
+  if (x > 1) p.radix[p.nf++] = x;
+  return p.nf <= kMaxFactors;
+}
+
+}  // namespace
+
+namespace kst {
+
+int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
+           const cplx* ub, int kb, int kind, int spatial_only, const double* dop_host, int D,
+           const cplx* grid_host, int G, int groups, double* values, cudaStream_t st) {
+  if (p < 1 || q < 1 || D < 1 || G < 1 || groups < 1 || G % groups)
+    return set_err(ctx, KST_ERR_DIMENSION, "detect: bad shape p=%d q=%d D=%d G=%d groups=%d", p, q,
+                   D, G, groups);
+  if (p > kMaxP) return set_err(ctx, KST_ERR_DIMENSION, "detect: p=%d exceeds %d", p, kMaxP);
+  if (ka < 0 || ka > p || kb < 0 || kb > std::min(q, kMaxKB))
+    return set_err(ctx, KST_ERR_DIMENSION, "detect: basis widths ka=%d kb=%d unsupported", ka, kb);
+  if (n == 0) return KST_OK;
+  const bool has_a = ua && ka > 0, has_b = ub && kb > 0;
+  int mode = 2, spatial = 0;
+  filter_mode(kind, has_a, has_b, spatial_only, mode, spatial);
+  const int kb_used = (mode == 2) ? 0 : kb;
+  bool uniform = true;
+  for (int d = 0; d < D && uniform; ++d) uniform = dop_host[d] == (double)d / (double)D;
+  Plan plan;
+  if (uniform && (!plan_factors(D, plan) || (size_t)3 * D * sizeof(cplx) > 200 * 1024)) uniform = false;
+  if (!uniform && (size_t)q * sizeof(cplx) > 200 * 1024)
+    return set_err(ctx, KST_ERR_DIMENSION, "detect: q=%d too long for the direct-sum path", q);
+
+  const int64_t rows = n * p;
+  // workspace: spec (rows x D), coef (rows x kb), ubspec (kb x D), ubT (kb x q),
+  // twiddles (D), hconj (G x p), dop (D), flag
+  const size_t bytes = sizeof(cplx) * ((size_t)rows * D + (size_t)rows * std::max(kb_used, 1) +
+                                       (size_t)std::max(kb_used, 1) * (D + q) + D + (size_t)G * p) +
+                       sizeof(double) * D + 256;
+  char* base = (char*)ws_get(ctx, WS_DET, bytes);
+  cplx* hstage = (cplx*)pinned_get(ctx, sizeof(cplx) * (size_t)G * p + sizeof(double) * D + 64);
+  if (!base || !hstage) return set_err(ctx, KST_ERR_CUDA, "detect: workspace");
+  cplx* spec = (cplx*)base;
+  cplx* coef = spec + (size_t)rows * D;
+  cplx* ubspec = coef + (size_t)rows * std::max(kb_used, 1);
+  cplx* ubT = ubspec + (size_t)std::max(kb_used, 1) * D;
+  cplx* tw = ubT + (size_t)std::max(kb_used, 1) * q;
+  cplx* hconj = tw + D;
+  double* dop = (double*)(hconj + (size_t)G * p);
+  int* flag = (int*)(dop + D);
+
+  // host staging of conj(grid) and dopplers
+  for (int e = 0; e < G * p; ++e) hstage[e] = cconj(grid_host[e]);
+  double* hdop = (double*)(hstage + (size_t)G * p);
+  for (int d = 0; d < D; ++d) hdop[d] = dop_host[d];
+  KST_CUDA(ctx, cudaMemcpyAsync(hconj, hstage, sizeof(cplx) * G * p, cudaMemcpyHostToDevice, st));
+  KST_CUDA(ctx, cudaMemcpyAsync(dop, hdop, sizeof(double) * D, cudaMemcpyHostToDevice, st));
+  KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));
+  if (uniform) {
+    KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_plan, &plan, sizeof(Plan), 0, cudaMemcpyHostToDevice, st));
+    twiddle_kernel<<<cdiv(D, 256), 256, 0, st>>>(tw, D);
+    KST_LAUNCH(ctx);
+  }
+  const size_t smem = uniform ? sizeof(cplx) * 3 * D : sizeof(cplx) * q;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    KST_CUDA(ctx, cudaFuncSetAttribute(row_spectrum_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    configured = 226 * 1024;
+  }
+  if (kb_used > 0) {
+    transpose_kernel<<<cdiv((int64_t)q * kb_used, 256), 256, 0, st>>>(ub, q, kb_used, ubT);
+    KST_LAUNCH(ctx);
+    // spectra of the temporal basis columns (coefficients unused)
+    row_spectrum_kernel<<<kb_used, NT, smem, st>>>(ubT, kb_used, q, nullptr, 0, tw, D, uniform, dop,
+                                                   ubspec, nullptr, flag + 1);
+    KST_LAUNCH(ctx);
+  }
+  row_spectrum_kernel<<<(unsigned)rows, NT, smem, st>>>(cube, rows, q, ub, kb_used, tw, D, uniform,
+                                                        dop, spec, coef, flag);
+  KST_LAUNCH(ctx);
+  CombineArgs a;
+  a.P = p;
+  a.D = D;
+  a.ka = has_a ? ka : 0;
+  a.kb = kb_used;
+  a.G = G;
+  a.groups = groups;
+  a.mode = mode;
+  a.spatial = spatial;
+  a.inv_sqrt_q = 1.0 / sqrt((double)q);
+  combine_kernel<<<dim3(cdiv(D, NT), (unsigned)n), NT, sizeof(cplx) * G * p, st>>>(
+      spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n);
+  KST_LAUNCH(ctx);
+  int hflag = 0;
+  KST_CUDA(ctx, cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KST_CUDA(ctx, cudaStreamSynchronize(st));
+  if (hflag) return set_err(ctx, KST_ERR_DATA, "bin matrix contains non-finite entries");
+  return KST_OK;
+}
+
+int filter_cube(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
+                const cplx* ub, int kb, int kind, int spatial_only, cplx* out, cudaStream_t st) {
+  if (p < 1 || q < 1 || p > kMaxP || ka < 0 || ka > p || kb < 0 || kb > std::min(q, kMaxKB))
+    return set_err(ctx, KST_ERR_DIMENSION, "filter: unsupported shape p=%d q=%d ka=%d kb=%d", p, q,
+                   ka, kb);
+  if (n == 0) return KST_OK;
+  const bool has_a = ua && ka > 0, has_b = ub && kb > 0;
+  int mode = 2, spatial = 0;
+  filter_mode(kind, has_a, has_b, spatial_only, mode, spatial);
+  const int kb_used = mode == 2 ? 0 : kb;
+  const int64_t rows = n * p;
+  char* base = (char*)ws_get(ctx, WS_DET, sizeof(cplx) * (size_t)rows * std::max(kb_used, 1) + 256);
+  if (!base) return set_err(ctx, KST_ERR_CUDA, "filter: workspace");
+  cplx* coef = (cplx*)base;
+  int* flag = (int*)(coef + (size_t)rows * std::max(kb_used, 1));
+  KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));
+  coef_kernel<<<(unsigned)rows, NT, 0, st>>>(cube, q, ub, kb_used, coef, flag);
+  KST_LAUNCH(ctx);
+  filter_apply_kernel<<<dim3(cdiv(q, NT), (unsigned)n), NT, 0, st>>>(
+      cube, coef, ub, has_a ? ua : coef, p, q, has_a ? ka : 0, kb_used, mode, spatial, out);
+  KST_LAUNCH(ctx);
+  int hflag = 0;
+  KST_CUDA(ctx, cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  KST_CUDA(ctx, cudaStreamSynchronize(st));
+  if (hflag) return set_err(ctx, KST_ERR_DATA, "bin matrix contains non-finite entries");
+  return KST_OK;
+}
+
+}  // namespace kst
+
+extern "C" int kst_filter(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
+                          const double* ua, int ka, const double* ub, int kb, int kind,
+                          int spatial_only, double* out, void* stream) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  ctx->err.clear();
+  return kst::filter_cube(ctx, (const cplx*)cube, n, p, q, (const cplx*)ua, ka, (const cplx*)ub, kb,
+                          kind, spatial_only, (cplx*)out, (cudaStream_t)stream);
+}
+
+extern "C" int kst_change(kst_ctx* ctx, const double* a, const double* b, int64_t count,
+                          int is_signed, double* out, void* stream) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  if (count <= 0) return KST_OK;
+  change_kernel<<<cdiv(count, 256) > 4096 ? 4096 : cdiv(count, 256), 256, 0, (cudaStream_t)stream>>>(
+      a, b, count, is_signed, out);
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}

@@ -1,0 +1,265 @@
+// K3: block-cooperative cyclic Jacobi for small complex Hermitian matrices
+// (n <= 64), FP64, in shared memory, with the reference's output
+// conventions (src/linalg.py:82-121): values descending; runs of values
+// within 1e-12 * max|lambda| re-ordered by each vector's dominant index
+// (stable); every vector rotated so its dominant entry is real positive.
+//
+// Parallel ordering: round-robin tournament, m/2 disjoint (p, q) pairs per
+// round; each round = rotation parameters -> column update (A and V) ->
+// row update (A), separated by __syncthreads.
+#pragma once
+#include "common.cuh"
+
+namespace kstj {
+
+constexpr int kMaxN = 64;
+
+__host__ __device__ inline int jac_ld(int n) { return ((n + 7) / 8) * 8 + 1; }
+
+// shared-memory layout needed by jacobi_smem for dimension n
+__host__ __device__ inline size_t jac_smem_bytes(int n) {
+  const int ld = jac_ld(n);
+  return sizeof(cplx) * 2 * (size_t)n * ld      // A, V
+         + sizeof(double) * 4 * (kMaxN / 2)     // c, s, cos/sin phase per pair
+         + sizeof(int) * 2 * (kMaxN / 2)        // p, q per pair
+         + sizeof(double) * 4 * kMaxN           // values, scratch, phase re/im
+         + sizeof(int) * 2 * kMaxN + 64;        // order, pivots, flags
+}
+
+struct JacSmem {
+  cplx* A;
+  cplx* V;
+  double *c, *s, *ec, *es;
+  int *pp, *pq;
+  double* val;
+  double* scratch;
+  double *phr, *phi;
+  int* order;
+  int* piv;
+  int* flag;
+  int ld;
+};
+
+__device__ inline JacSmem jac_carve(void* base, int n) {
+  JacSmem j;
+  j.ld = jac_ld(n);
+  char* p = (char*)base;
+  j.A = (cplx*)p;
+  p += sizeof(cplx) * (size_t)n * j.ld;
+  j.V = (cplx*)p;
+  p += sizeof(cplx) * (size_t)n * j.ld;
+  j.c = (double*)p;
+  j.s = j.c + kMaxN / 2;
+  j.ec = j.s + kMaxN / 2;
+  j.es = j.ec + kMaxN / 2;
+  p += sizeof(double) * 4 * (kMaxN / 2);
+  j.pp = (int*)p;
+  j.pq = j.pp + kMaxN / 2;
+  p += sizeof(int) * 2 * (kMaxN / 2);
+  j.val = (double*)p;
+  j.scratch = j.val + kMaxN;
+  j.phr = j.scratch + kMaxN;
+  j.phi = j.phr + kMaxN;
+  p += sizeof(double) * 4 * kMaxN;
+  j.order = (int*)p;
+  j.piv = j.order + kMaxN;
+  j.flag = j.piv + kMaxN;
+  return j;
+}
+
+// Load (M/div + (M/div)^H)/2 into A, V = I. M: global or shared, row-major,
+// leading dim ldm. div reproduces e.g. eig_truncate(v / |b|^2) (src/lrkron.py:207).
+__device__ inline void jac_load_sym(JacSmem& j, const cplx* M, int ldm, int n, double div) {
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int r = e / n, c = e % n;
+    const cplx x = M[(size_t)r * ldm + c], y = M[(size_t)c * ldm + r];
+    // (x + conj(y)) / 2, matching the reference's symmetrisation order
+    j.A[r * j.ld + c] = cmk(((x.x / div) + (y.x / div)) / 2.0, ((x.y / div) - (y.y / div)) / 2.0);
+    j.V[r * j.ld + c] = cmk(r == c ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+}
+
+// Run Jacobi sweeps on j.A (Hermitian), accumulating j.V. On return
+// j.val holds the (unsorted) diagonal.
+__device__ inline void jac_sweeps(JacSmem& j, int n) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (n == 1) {
+    if (tid == 0) j.val[0] = j.A[0].x;
+    __syncthreads();
+    return;
+  }
+  const int m = (n + 1) & ~1;  // even player count (index n is a bye when n is odd)
+  const int npairs = m / 2;
+  // Frobenius norm for the absolute rotation floor
+  if (tid == 0) {
+    double f = 0.0;
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < n; ++c) f += cabs2(j.A[r * j.ld + c]);
+    j.scratch[0] = sqrt(f);
+  }
+  __syncthreads();
+  const double fro = j.scratch[0];
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) *j.flag = 0;
+    __syncthreads();
+    for (int round = 0; round < m - 1; ++round) {
+      // tournament pairing: player 0 fixed, others rotate
+      if (tid < npairs) {
+        int a, b;
+        if (tid == 0) {
+          a = 0;
+          b = 1 + (round % (m - 1));
+        } else {
+          a = 1 + ((round + tid) % (m - 1));
+          b = 1 + ((round + m - 1 - tid) % (m - 1));
+        }
+        if (a > b) {
+          int t = a;
+          a = b;
+          b = t;
+        }
+        double c = 1.0, s = 0.0, ec = 1.0, es = 0.0;
+        if (b < n) {
+          const double app = j.A[a * j.ld + a].x, aqq = j.A[b * j.ld + b].x;
+          const cplx apq = j.A[a * j.ld + b];
+          const double r = hypot(apq.x, apq.y);
+          const double thr = fmax(1e-17 * sqrt(fabs(app) * fabs(aqq)), 1e-300 + 1e-18 * fro);
+          if (r > thr) {
+            ec = apq.x / r;
+            es = apq.y / r;  // e^{i phi}
+            const double tau = (aqq - app) / (2.0 * r);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            // post-rotation diagonal (exact 2x2 values)
+            j.scratch[2 * tid] = app - t * r;
+            j.scratch[2 * tid + 1] = aqq + t * r;
+            *j.flag = 1;
+          }
+        }
+        j.pp[tid] = a;
+        j.pq[tid] = b;
+        j.c[tid] = c;
+        j.s[tid] = s;
+        j.ec[tid] = ec;
+        j.es[tid] = es;
+      }
+      __syncthreads();
+      // column update: A <- A U, V <- V U on columns (p, q)
+      for (int e = tid; e < npairs * n * 2; e += nt) {
+        const int mat = e / (npairs * n);
+        const int rem = e - mat * npairs * n;
+        const int k = rem / n, row = rem % n;
+        const int p = j.pp[k], q = j.pq[k];
+        if (q >= n || j.s[k] == 0.0) continue;
+        cplx* M = mat ? j.V : j.A;
+        const double c = j.c[k], s = j.s[k];
+        const cplx emi = cmk(j.ec[k], -j.es[k]);  // e^{-i phi}
+        const cplx xp = M[row * j.ld + p], xq = M[row * j.ld + q];
+        const cplx wq = cmul(emi, xq);
+        M[row * j.ld + p] = cmk(c * xp.x - s * wq.x, c * xp.y - s * wq.y);
+        M[row * j.ld + q] = cmk(s * xp.x + c * wq.x, s * xp.y + c * wq.y);
+      }
+      __syncthreads();
+      // row update: A <- U^H A on rows (p, q)
+      for (int e = tid; e < npairs * n; e += nt) {
+        const int k = e / n, col = e % n;
+        const int p = j.pp[k], q = j.pq[k];
+        if (q >= n || j.s[k] == 0.0) continue;
+        const double c = j.c[k], s = j.s[k];
+        const cplx epi = cmk(j.ec[k], j.es[k]);  // e^{i phi}
+        const cplx xp = j.A[p * j.ld + col], xq = j.A[q * j.ld + col];
+        const cplx wq = cmul(epi, xq);
+        j.A[p * j.ld + col] = cmk(c * xp.x - s * wq.x, c * xp.y - s * wq.y);
+        j.A[q * j.ld + col] = cmk(s * xp.x + c * wq.x, s * xp.y + c * wq.y);
+      }
+      __syncthreads();
+      if (tid < npairs) {
+        const int p = j.pp[tid], q = j.pq[tid];
+        if (q < n && j.s[tid] != 0.0) {
+          j.A[p * j.ld + p] = cmk(j.scratch[2 * tid], 0.0);
+          j.A[q * j.ld + q] = cmk(j.scratch[2 * tid + 1], 0.0);
+          j.A[p * j.ld + q] = cmk(0.0, 0.0);
+          j.A[q * j.ld + p] = cmk(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+    }
+    const int any = *j.flag;
+    __syncthreads();
+    if (!any) break;
+  }
+  for (int i = tid; i < n; i += nt) j.val[i] = j.A[i * j.ld + i].x;
+  __syncthreads();
+}
+
+// Descending order + tie rule + pivot phase. Produces j.order (column of V
+// for output position k) and rotates V's columns in place.
+__device__ inline void jac_finish(JacSmem& j, int n) {
+  const int tid = threadIdx.x;
+  // pivot (first argmax |v_ik|) of every column
+  for (int k = tid; k < n; k += blockDim.x) {
+    int best = 0;
+    double bm = -1.0;
+    for (int i = 0; i < n; ++i) {
+      const cplx v = j.V[i * j.ld + k];
+      const double a = hypot(v.x, v.y);
+      if (a > bm) {
+        bm = a;
+        best = i;
+      }
+    }
+    j.piv[k] = best;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int k = 0; k < n; ++k) j.order[k] = k;
+    // stable insertion sort, descending by value
+    for (int a = 1; a < n; ++a) {
+      const int key = j.order[a];
+      int b = a - 1;
+      while (b >= 0 && j.val[j.order[b]] < j.val[key]) {
+        j.order[b + 1] = j.order[b];
+        --b;
+      }
+      j.order[b + 1] = key;
+    }
+    double mx = 0.0;
+    for (int k = 0; k < n; ++k) mx = fmax(mx, fabs(j.val[k]));
+    const double tie = mx * 1e-12;
+    int s = 0;
+    while (s < n) {
+      int e = s + 1;
+      while (e < n && fabs(j.val[j.order[e]] - j.val[j.order[e - 1]]) <= tie) ++e;
+      if (e - s > 1) {  // stable sort of the run by dominant index
+        for (int a = s + 1; a < e; ++a) {
+          const int key = j.order[a];
+          int b = a - 1;
+          while (b >= s && j.piv[j.order[b]] > j.piv[key]) {
+            j.order[b + 1] = j.order[b];
+            --b;
+          }
+          j.order[b + 1] = key;
+        }
+      }
+      s = e;
+    }
+  }
+  __syncthreads();
+  // pivot phase: v_k *= conj(z)/|z|, z = v[piv_k, k] (factors first, then apply)
+  for (int k = tid; k < n; k += blockDim.x) {
+    const cplx z = j.V[j.piv[k] * j.ld + k];
+    const double mag = hypot(z.x, z.y);
+    j.phr[k] = mag > 0.0 ? z.x / mag : 1.0;
+    j.phi[k] = mag > 0.0 ? -z.y / mag : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, k = e % n;
+    j.V[i * j.ld + k] = cmul(j.V[i * j.ld + k], cmk(j.phr[k], j.phi[k]));
+  }
+  __syncthreads();
+}
+
+}  // namespace kstj

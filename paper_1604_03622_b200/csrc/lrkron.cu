@@ -1,0 +1,458 @@
+// K2 + K3: the LR-Kron alternating estimator, `lr_kron_estimate`
+// (src/lrkron.py:118-230), on a device-resident covariance S (pq x pq).
+//
+// Streaming passes over S (HBM-bound), with S4[i,r,j,c] =
+// S[i*q + r, j*q + c]:
+//   stats  : |S|_F^2, block sums A0 = sum_rc S4 / q^2, non-finite count,
+//            diagonal min/max                     (src/lrkron.py:100-115,151,173-175)
+//   b-step : b[r,c] = sum_ij S4[i,r,j,c] conj(A[i,j]) / |A|^2, plus |b|^2 partials
+//                                                  (src/lrkron.py:185-195)
+//   V-step : V[i,j] = sum_rc S4[i,r,j,c] conj(b[r,c])  (src/lrkron.py:197-205)
+//   tail   : one CTA: A = EIG_ra(V / |b|^2) by Jacobi, expanded-norm residual,
+//            stall test                           (src/lrkron.py:207-221)
+// Every reduction is per-CTA partials + one fixed-order pass: bitwise
+// reproducible. The final temporal factor is EIG_rb(b) (src/lrkron.py:223),
+// computed once by heig_top and reused by build_filter.
+#include <algorithm>
+
+#include "jacobi.cuh"
+
+namespace {
+
+using namespace kstj;
+
+constexpr int NT = 256;
+constexpr int kMaxP = 16;
+constexpr int ST_ROWS = 8;   // rows of S per stats CTA
+constexpr int V_ROWS = 8;    // rows of S per V-step CTA
+
+// partial layout per CTA: [fro2, nonfinite, dmin, dmax, blocksum(j).re/im ...]
+__global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, int P, int q,
+                                                   double* __restrict__ part) {
+  __shared__ double sh[32];
+  const int64_t d = (int64_t)P * q;
+  const int i = blockIdx.y;                    // block row
+  const int r0 = blockIdx.x * ST_ROWS;         // row within block
+  const int rows = min(ST_ROWS, q - r0);
+  double fro = 0.0, bad = 0.0, dmin = 1e308, dmax = -1e308;
+  double bs[2 * kMaxP];
+#pragma unroll
+  for (int j = 0; j < 2 * kMaxP; ++j) bs[j] = 0.0;
+  for (int rr = 0; rr < rows; ++rr) {
+    const int64_t a = (int64_t)i * q + r0 + rr;
+    const cplx* row = S + a * d;
+#pragma unroll
+    for (int j = 0; j < kMaxP; ++j) {
+      if (j >= P) break;
+      double sr = 0.0, si = 0.0;
+      for (int c = threadIdx.x; c < q; c += NT) {
+        const cplx v = row[(int64_t)j * q + c];
+        if (!isfinite(v.x) || !isfinite(v.y)) bad += 1.0;
+        fro = fma(v.x, v.x, fro);
+        fro = fma(v.y, v.y, fro);
+        sr += v.x;
+        si += v.y;
+      }
+      bs[2 * j] += sr;
+      bs[2 * j + 1] += si;
+    }
+    if (threadIdx.x == 0) {
+      const double dv = row[a].x;
+      dmin = fmin(dmin, dv);
+      dmax = fmax(dmax, dv);
+    }
+  }
+  double* out = part + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * (4 + 2 * kMaxP);
+  fro = block_sum<NT>(fro, sh);
+  bad = block_sum<NT>(bad, sh);
+  if (threadIdx.x == 0) {
+    out[0] = fro;
+    out[1] = bad;
+    out[2] = dmin;
+    out[3] = dmax;
+  }
+  for (int j = 0; j < 2 * P; ++j) {
+    const double v = block_sum<NT>(bs[j], sh);
+    if (threadIdx.x == 0) out[4 + j] = v;
+  }
+}
+
+// State block shared by the iteration kernels (device memory).
+struct IterState {
+  double fro, fro2, na2, nb2, eta_prev, eta;
+  int status;      // 0 ok, KST_ERR_DATA / KST_ERR_DEGENERATE
+  int converged;
+  int iteration;
+  int pad;
+  cplx A[kMaxP * kMaxP];   // current spatial iterate (row-major P x P)
+  cplx Ainv[kMaxP * kMaxP];  // conj(A) / |A|^2 (b-step operand)
+};
+
+// Reduce stats partials -> fro, A0 (= blocksum / q^2), |A0|^2; diag checks.
+__global__ void init_kernel(const double* __restrict__ part, int nblk_x, int P, int q,
+                            IterState* st, double* host_diag) {
+  // single thread: fixed order
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double fro2 = 0.0, bad = 0.0, dmin = 1e308, dmax = -1e308;
+  for (int i = 0; i < P; ++i) {
+    double bsr[kMaxP], bsi[kMaxP];
+    for (int j = 0; j < P; ++j) bsr[j] = bsi[j] = 0.0;
+    for (int x = 0; x < nblk_x; ++x) {
+      const double* o = part + (size_t)(i * nblk_x + x) * (4 + 2 * kMaxP);
+      fro2 += o[0];
+      bad += o[1];
+      dmin = fmin(dmin, o[2]);
+      dmax = fmax(dmax, o[3]);
+      for (int j = 0; j < P; ++j) {
+        bsr[j] += o[4 + 2 * j];
+        bsi[j] += o[4 + 2 * j + 1];
+      }
+    }
+    for (int j = 0; j < P; ++j)
+      st->A[i * P + j] = cmk(bsr[j] / (double)(q * (double)q), bsi[j] / (double)(q * (double)q));
+  }
+  double na2 = 0.0;
+  for (int e = 0; e < P * P; ++e) na2 += cabs2(st->A[e]);
+  st->fro2 = fro2;
+  st->fro = sqrt(fro2);
+  st->na2 = na2;
+  st->eta_prev = INFINITY;
+  st->status = 0;
+  st->converged = 0;
+  st->iteration = 0;
+  for (int e = 0; e < P * P; ++e)
+    st->Ainv[e] = cmk(st->A[e].x, -st->A[e].y);
+  host_diag[0] = bad;
+  host_diag[1] = dmin;
+  host_diag[2] = dmax;
+  host_diag[3] = st->fro;
+  host_diag[4] = na2;
+}
+
+// b[r,c] = sum_ij S4[i,r,j,c] conj(A[i,j]) / |A|^2 ; partial |b|^2 per CTA
+__global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, int P, int q,
+                                                   const IterState* __restrict__ st,
+                                                   cplx* __restrict__ b, double* __restrict__ part) {
+  __shared__ cplx ca[kMaxP * kMaxP];
+  __shared__ double sh[32];
+  for (int e = threadIdx.x; e < P * P; e += NT) ca[e] = st->Ainv[e];
+  __syncthreads();
+  const double na2 = st->na2;
+  const int64_t d = (int64_t)P * q;
+  const int r = blockIdx.y;
+  const int c = blockIdx.x * NT + threadIdx.x;
+  double nb = 0.0;
+  if (c < q) {
+    cplx acc = cmk(0, 0);
+    for (int i = 0; i < P; ++i) {
+      const cplx* row = S + ((int64_t)i * q + r) * d + c;
+      for (int j = 0; j < P; ++j) cfma(acc, row[(int64_t)j * q], ca[i * P + j]);
+    }
+    acc = cmk(acc.x / na2, acc.y / na2);
+    b[(int64_t)r * q + c] = acc;
+    nb = cabs2(acc);
+  }
+  nb = block_sum<NT>(nb, sh);
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = nb;
+}
+
+// V partials: CTA (x = row chunk, y = block row i) -> part[(i, x)][j]
+__global__ void __launch_bounds__(NT) vstep_kernel(const cplx* __restrict__ S, int P, int q,
+                                                   const cplx* __restrict__ b,
+                                                   cplx* __restrict__ part) {
+  __shared__ double sh[32];
+  const int64_t d = (int64_t)P * q;
+  const int i = blockIdx.y;
+  const int r0 = blockIdx.x * V_ROWS;
+  const int rows = min(V_ROWS, q - r0);
+  double ar[kMaxP], ai[kMaxP];
+#pragma unroll
+  for (int j = 0; j < kMaxP; ++j) ar[j] = ai[j] = 0.0;
+  for (int rr = 0; rr < rows; ++rr) {
+    const int r = r0 + rr;
+    const cplx* row = S + ((int64_t)i * q + r) * d;
+    const cplx* brow = b + (int64_t)r * q;
+    for (int c = threadIdx.x; c < q; c += NT) {
+      const cplx bv = brow[c];
+#pragma unroll
+      for (int j = 0; j < kMaxP; ++j) {
+        if (j < P) {
+          const cplx s = row[(int64_t)j * q + c];
+          // s * conj(bv)
+          ar[j] = fma(s.x, bv.x, ar[j]);
+          ar[j] = fma(s.y, bv.y, ar[j]);
+          ai[j] = fma(s.y, bv.x, ai[j]);
+          ai[j] = fma(-s.x, bv.y, ai[j]);
+        }
+      }
+    }
+  }
+  cplx* out = part + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * P;
+  for (int j = 0; j < P; ++j) {
+    const double re = block_sum<NT>(ar[j], sh);
+    const double im = block_sum<NT>(ai[j], sh);
+    if (threadIdx.x == 0) out[j] = cmk(re, im);
+  }
+}
+
+// One CTA: reduce V and |b|^2, spatial truncation, residual, stall test.
+__global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart, int nvx,
+                                                  const double* __restrict__ bpart, int nbp,
+                                                  int P, int ra, double tol, IterState* st,
+                                                  cplx* __restrict__ spatial_out,
+                                                  double* __restrict__ host_out) {
+  extern __shared__ __align__(16) char sm[];
+  __shared__ cplx V[kMaxP * kMaxP];
+  __shared__ cplx Anew[kMaxP * kMaxP];
+  __shared__ double lam[kMaxP];
+  __shared__ double nb2_s;
+  __shared__ int bad_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    double nb2 = 0.0;
+    for (int k = 0; k < nbp; ++k) nb2 += bpart[k];
+    nb2_s = nb2;
+  }
+  for (int e = tid; e < P * P; e += NT) {
+    const int i = e / P, j = e % P;
+    cplx acc = cmk(0, 0);
+    for (int x = 0; x < nvx; ++x) acc = cadd(acc, vpart[(size_t)(i * nvx + x) * P + j]);
+    V[e] = acc;
+  }
+  __syncthreads();
+  const double nb2 = nb2_s;
+  if (nb2 == 0.0) {
+    if (tid == 0) {
+      st->status = KST_ERR_DEGENERATE;
+      host_out[0] = KST_ERR_DEGENERATE;
+    }
+    return;
+  }
+  // eig_truncate(V / nb2, ra): Hermitian check first (src/linalg.py:68-79)
+  if (tid == 0) {
+    double f = 0.0, a = 0.0;
+    for (int r = 0; r < P; ++r)
+      for (int c = 0; c < P; ++c) {
+        const cplx x = cmk(V[r * P + c].x / nb2, V[r * P + c].y / nb2);
+        const cplx y = cmk(V[c * P + r].x / nb2, V[c * P + r].y / nb2);
+        f += cabs2(x);
+        a += cabs2(cmk(x.x - y.x, x.y + y.y));
+        if (!isfinite(x.x) || !isfinite(x.y)) a = INFINITY;
+      }
+    bad_s = (sqrt(f) > 0 && !(sqrt(a) <= 1e-8 * sqrt(f))) ? 1 : 0;
+  }
+  __syncthreads();
+  if (bad_s) {
+    if (tid == 0) {
+      st->status = KST_ERR_DATA;
+      host_out[0] = KST_ERR_DATA;
+    }
+    return;
+  }
+  if (ra == P) {
+    for (int e = tid; e < P * P; e += NT) {
+      const int r = e / P, c = e % P;
+      const cplx x = V[r * P + c], y = V[c * P + r];
+      Anew[e] = cmk(((x.x / nb2) + (y.x / nb2)) / 2.0, ((x.y / nb2) - (y.y / nb2)) / 2.0);
+    }
+  } else {
+    JacSmem j = jac_carve(sm, P);
+    jac_load_sym(j, V, P, P, nb2);
+    jac_sweeps(j, P);
+    jac_finish(j, P);
+    if (tid == 0) {
+      double top = 0.0;
+      for (int k = 0; k < P; ++k) top = fmax(top, fabs(j.val[k]));
+      for (int k = 0; k < ra; ++k) {
+        double v = j.val[j.order[k]];
+        if (v < 0 && fabs(v) <= 1e-10 * top) v = 0.0;
+        lam[k] = v;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < P * P; e += NT) {
+      const int a = e / P, c = e % P;
+      cplx ab = cmk(0, 0), ba = cmk(0, 0);
+      for (int k = 0; k < ra; ++k) {
+        const cplx ua = j.V[a * j.ld + j.order[k]], uc = j.V[c * j.ld + j.order[k]];
+        cfmac(ab, cscale(ua, lam[k]), uc);
+        cfmac(ba, cscale(uc, lam[k]), ua);
+      }
+      Anew[e] = cmk((ab.x + ba.x) / 2.0, (ab.y - ba.y) / 2.0);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double cross = 0.0, na2 = 0.0;
+    for (int e = 0; e < P * P; ++e) {
+      cross += Anew[e].x * V[e].x + Anew[e].y * V[e].y;  // Re vdot(A, V)
+      na2 += cabs2(Anew[e]);
+    }
+    const double fro = st->fro;
+    const double eta2 = st->fro2 + na2 * nb2 - 2.0 * cross;
+    const double eta = sqrt(fmax(eta2, 0.0)) / fro;
+    const int conv = fabs(st->eta_prev - eta) <= tol;
+    st->eta_prev = eta;
+    st->eta = eta;
+    st->nb2 = nb2;
+    st->na2 = na2;
+    st->converged = conv;
+    st->iteration += 1;
+    for (int e = 0; e < P * P; ++e) {
+      st->A[e] = Anew[e];
+      spatial_out[e] = Anew[e];
+      st->Ainv[e] = cmk(Anew[e].x, -Anew[e].y);
+    }
+    host_out[0] = 0;
+    host_out[1] = eta;
+    host_out[2] = conv;
+    host_out[3] = na2;
+  }
+}
+
+__global__ void zero_kernel(cplx* p, int64_t count) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = cmk(0, 0);
+}
+
+}  // namespace
+
+namespace kst {
+
+int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol, int max_iter,
+           int validate, cplx* spatial, cplx* temporal, cplx* tb_vectors, double* tb_values,
+           FitOut* fit, cplx* iter_spatial, cplx* iter_b, cudaStream_t st) {
+  if (p < 1 || q < 1) return set_err(ctx, KST_ERR_DIMENSION, "block shape must be positive");
+  if (p > kMaxP) return set_err(ctx, KST_ERR_DIMENSION, "p=%d exceeds the supported %d channels", p, kMaxP);
+  const int64_t d = (int64_t)p * q;
+  // stats pass
+  const int nbx = (q + ST_ROWS - 1) / ST_ROWS;
+  const size_t stat_stride = 4 + 2 * kMaxP;
+  const int nvx = (q + V_ROWS - 1) / V_ROWS;
+  const int nbb = (q + NT - 1) / NT;
+  char* small = (char*)ws_get(ctx, WS_SMALL, sizeof(IterState) + 256);
+  double* part = (double*)ws_get(
+      ctx, WS_PART,
+      std::max(sizeof(double) * stat_stride * p * nbx,
+               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64));
+  cplx* b = (cplx*)ws_get(ctx, WS_B, sizeof(cplx) * (size_t)q * q);
+  double* hbuf = (double*)pinned_get(ctx, 64 * sizeof(double));
+  if (!small || !part || !b || !hbuf) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");
+  IterState* state = (IterState*)small;
+
+  stats_kernel<<<dim3(nbx, p), NT, 0, st>>>(S, p, q, part);
+  KST_LAUNCH(ctx);
+  init_kernel<<<1, 32, 0, st>>>(part, nbx, p, q, state, (double*)(small + sizeof(IterState)));
+  KST_LAUNCH(ctx);
+  KST_CUDA(ctx, cudaMemcpyAsync(hbuf, small + sizeof(IterState), 5 * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+  KST_CUDA(ctx, cudaStreamSynchronize(st));
+  const double bad = hbuf[0], dmin = hbuf[1], dmax = hbuf[2], fro = hbuf[3];
+  double na2 = hbuf[4];
+  if (bad > 0) return set_err(ctx, KST_ERR_DATA, "covariance contains non-finite entries");
+  if (validate) {
+    KST_TRY(herm_check(ctx, S, (int)d, st));
+    if (dmin < -1e-8 * std::max(dmax, 0.0))
+      return set_err(ctx, KST_ERR_DATA, "covariance has a negative diagonal, not PSD");
+  }
+  if (ra < 1 || ra > p)
+    return set_err(ctx, KST_ERR_DIMENSION, "spatial rank must be in [1, %d], got %d", p, ra);
+  if (rb < 1 || rb > q)
+    return set_err(ctx, KST_ERR_DIMENSION, "temporal rank must be in [1, %d], got %d", q, rb);
+  if (max_iter < 1) return set_err(ctx, KST_ERR_DIMENSION, "max_iter must be >= 1, got %d", max_iter);
+
+  fit->residuals.clear();
+  if (fro == 0.0) {
+    zero_kernel<<<1, 256, 0, st>>>(spatial, (int64_t)p * p);
+    KST_LAUNCH(ctx);
+    if (temporal) {
+      zero_kernel<<<cdiv((int64_t)q * q, 256), 256, 0, st>>>(temporal, (int64_t)q * q);
+      KST_LAUNCH(ctx);
+    }
+    fit->iterations = 0;
+    fit->converged = 1;
+    fit->residuals.push_back(0.0);
+    fit->n_res = 1;
+    if (tb_values)
+      for (int k = 0; k < rb; ++k) tb_values[k] = 0.0;
+    KST_CUDA(ctx, cudaStreamSynchronize(st));
+    return KST_OK;
+  }
+
+  cplx* vpart = (cplx*)part;
+  double* bpart = (double*)(vpart + (size_t)p * nvx * p);
+  double* hout = (double*)(small + sizeof(IterState) + 64);
+  const size_t tail_smem = jac_smem_bytes(p);
+  int iters = 0, conv = 0;
+  for (int it = 0; it < max_iter; ++it) {
+    if (na2 == 0.0) return set_err(ctx, KST_ERR_DEGENERATE, "spatial iterate collapsed to zero");
+    ++iters;
+    bstep_kernel<<<dim3(nbb, q), NT, 0, st>>>(S, p, q, state, b, bpart);
+    KST_LAUNCH(ctx);
+    vstep_kernel<<<dim3(nvx, p), NT, 0, st>>>(S, p, q, b, vpart);
+    KST_LAUNCH(ctx);
+    tail_kernel<<<1, NT, tail_smem, st>>>(vpart, nvx, bpart, nbb * q, p, ra, tol, state, spatial, hout);
+    KST_LAUNCH(ctx);
+    KST_CUDA(ctx, cudaMemcpyAsync(hbuf, hout, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (iter_spatial)
+      KST_CUDA(ctx, cudaMemcpyAsync(iter_spatial + (size_t)it * p * p, spatial,
+                                    sizeof(cplx) * p * p, cudaMemcpyDeviceToDevice, st));
+    if (iter_b)
+      KST_CUDA(ctx, cudaMemcpyAsync(iter_b + (size_t)it * q * q, b, sizeof(cplx) * (size_t)q * q,
+                                    cudaMemcpyDeviceToDevice, st));
+    KST_CUDA(ctx, cudaStreamSynchronize(st));
+    const int status = (int)hbuf[0];
+    if (status == KST_ERR_DEGENERATE)
+      return set_err(ctx, KST_ERR_DEGENERATE, "temporal iterate collapsed to zero");
+    if (status == KST_ERR_DATA)
+      return set_err(ctx, KST_ERR_DATA, "matrix deviates from Hermitian beyond tolerance");
+    fit->residuals.push_back(hbuf[1]);
+    na2 = hbuf[3];
+    if (hbuf[2] != 0.0) {
+      conv = 1;
+      break;
+    }
+  }
+  fit->iterations = iters;
+  fit->converged = conv;
+  fit->n_res = (int)fit->residuals.size();
+
+  // temporal = EIG_rb(b)   (src/lrkron.py:223)
+  if (validate) KST_TRY(herm_check(ctx, b, q, st));
+  if (rb == q) {
+    if (temporal) {
+      // (b + b^H)/2 without eig (src/linalg.py:135-136)
+      KST_TRY(eig_truncate(ctx, b, q, q, temporal, st));
+    }
+    return KST_OK;
+  }
+  const int want = q <= kMaxN ? q : rb;
+  std::vector<double> vals(want);
+  cplx* U = (cplx*)ws_get(ctx, WS_UB, sizeof(cplx) * (size_t)q * want);
+  if (!U) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");
+  KST_TRY(heig_top(ctx, b, q, want, vals.data(), U, st));
+  double top = 0.0;
+  for (int k = 0; k < want; ++k) top = std::max(top, std::fabs(vals[k]));
+  cplx* Ur = U;
+  if (want != rb) {
+    Ur = tb_vectors ? tb_vectors : (cplx*)ws_get(ctx, WS_EIG2, sizeof(cplx) * (size_t)q * rb);
+    KST_CUDA(ctx, cudaMemcpy2DAsync(Ur, sizeof(cplx) * rb, U, sizeof(cplx) * want,
+                                    sizeof(cplx) * rb, q, cudaMemcpyDeviceToDevice, st));
+  } else if (tb_vectors) {
+    KST_CUDA(ctx, cudaMemcpyAsync(tb_vectors, U, sizeof(cplx) * (size_t)q * rb,
+                                  cudaMemcpyDeviceToDevice, st));
+    Ur = tb_vectors;
+  }
+  if (tb_values)
+    for (int k = 0; k < rb; ++k) {
+      double v = vals[k];
+      if (v < 0 && std::fabs(v) <= 1e-10 * top) v = 0.0;
+      tb_values[k] = v;
+    }
+  if (temporal) KST_TRY(truncate_from_pairs(ctx, vals.data(), Ur, q, rb, top, temporal, st));
+  KST_CUDA(ctx, cudaStreamSynchronize(st));
+  return KST_OK;
+}
+
+}  // namespace kst

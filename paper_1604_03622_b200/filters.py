@@ -1,0 +1,231 @@
+"""Clutter-cancellation filters and detection maps on the GPU.
+
+Mirrors `kronstap.filters` (src/filters.py) for the projection filters:
+`subspace_basis`, `StapFilter`, `projection_filter`, `build_filter`,
+`detection_image`, `DetectionMap` and the grids. Kernels: kst_subspace_basis
+(K3/K4), kst_detect (K5), kst_filter (whole-cube apply_matrix).
+
+Out of scope: the "optimal" (Cholesky-whitening) kind,
+steering / SINR helpers -- they are not on the image path. They raise
+NotImplementedError here instead of silently running on the CPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from ._dual import Dual
+from .errors import DimensionError
+from .linalg import subspace_basis_device
+
+FILTER_KINDS = ("optimal", "classical", "kron")
+
+
+def _basis_dual(b):
+    if b is None or isinstance(b, Dual):
+        return b
+    return Dual(b)
+
+
+def subspace_basis(matrix, rank, tol=1e-9):
+    """Orthonormal basis of the top eigen-subspace, or None (src/filters.py:58-73)."""
+    out = subspace_basis_device(matrix, rank, tol)
+    if out is None:
+        return None
+    return out if nat.is_device(matrix) else nat.to_host(out)
+
+
+class StapFilter:
+    """Factored clutter filter for p-channel, q-pulse snapshots (src/filters.py:76-120).
+
+    Bases may be numpy arrays or CUDA tensors; they are uploaded once."""
+
+    def __init__(self, kind, p, q, spatial_basis=None, temporal_basis=None, spatial_only=False):
+        self.kind = kind
+        self.p = p
+        self.q = q
+        self._ua = _basis_dual(spatial_basis)
+        self._ub = _basis_dual(temporal_basis)
+        self.spatial_only = spatial_only
+
+    @property
+    def spatial_basis(self):
+        return None if self._ua is None else self._ua.value()
+
+    @spatial_basis.setter
+    def spatial_basis(self, v):
+        self._ua = _basis_dual(v)
+
+    @property
+    def temporal_basis(self):
+        return None if self._ub is None else self._ub.value()
+
+    @temporal_basis.setter
+    def temporal_basis(self, v):
+        self._ub = _basis_dual(v)
+
+    def _dev_bases(self):
+        ua = None if self._ua is None else self._ua.dev()
+        ub = None if self._ub is None else self._ub.dev()
+        return ua, ub
+
+    def _kind_code(self):
+        if self.kind == "optimal":
+            raise NotImplementedError("the 'optimal' filter kind is out of scope for the GPU path")
+        if self.kind not in nat.KIND:
+            raise DimensionError(f"unknown filter kind {self.kind!r}")
+        return nat.KIND[self.kind]
+
+    def apply_cube(self, cube):
+        """Filter every bin of an (n, p, q) cube (kst_filter)."""
+        import torch
+        shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
+        if len(shp) != 3 or shp[1:] != (self.p, self.q):
+            raise DimensionError(f"cube shape {shp} does not match filter ({self.p}, {self.q})")
+        kind = self._kind_code()
+        x = nat.to_device(cube)
+        ua, ub = self._dev_bases()
+        out = torch.empty_like(x)
+        c = nat.ctx(x.device)
+        nat.check(nat.lib().kst_filter(
+            c, nat.ptr(x), shp[0], self.p, self.q, nat.ptr(ua), 0 if ua is None else ua.shape[1],
+            nat.ptr(ub), 0 if ub is None else ub.shape[1], kind, int(bool(self.spatial_only)),
+            nat.ptr(out), nat.stream_of(x.device)), c)
+        return out if nat.is_device(cube) else nat.to_host(out)
+
+    def apply_matrix(self, x):
+        """Filter one bin given as its (p, q) matrix (src/filters.py:88-116)."""
+        shp = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
+        if len(shp) != 2:
+            raise DimensionError(f"bin matrix must be 2-D, got shape {shp}")
+        if shp != (self.p, self.q):
+            raise DimensionError(f"bin shape {shp} does not match filter ({self.p}, {self.q})")
+        out = self.apply_cube(x.reshape(1, self.p, self.q) if nat.is_device(x)
+                              else np.asarray(x, dtype=np.complex128).reshape(1, self.p, self.q))
+        return out[0]
+
+    def apply(self, x):
+        """Filter one channel-major snapshot vector (src/filters.py:118-120)."""
+        v = x.reshape(-1) if nat.is_device(x) else np.asarray(x).ravel()
+        if v.shape[0] != self.p * self.q:
+            raise DimensionError(f"snapshot length {v.shape[0]} does not match {self.p}x{self.q}")
+        return self.apply_matrix(v.reshape(self.p, self.q)).reshape(-1)
+
+
+def projection_filter(kind, spatial_basis, temporal_basis, p, q, spatial_only=False):
+    """src/filters.py:123-134."""
+    if kind not in ("classical", "kron"):
+        raise DimensionError(f"unknown projection filter kind {kind!r}")
+    for name, basis, dim in (("spatial", spatial_basis, p), ("temporal", temporal_basis, q)):
+        if basis is not None and basis.shape[0] != dim:
+            raise DimensionError(f"{name} basis has {basis.shape[0]} rows, expected {dim}")
+    return StapFilter(kind, p, q, spatial_basis, temporal_basis, spatial_only)
+
+
+def build_filter(kind, estimate=None, sigma=None, p=None, q=None, drop_temporal=False, rank_tol=1e-9):
+    """src/filters.py:137-175. The temporal basis reuses the eigenpairs the
+    estimator already computed for `temporal` (one q x q eigensolve, not two)."""
+    if kind not in FILTER_KINDS:
+        raise DimensionError(f"unknown filter kind {kind!r}")
+    if kind == "optimal":
+        raise NotImplementedError("the 'optimal' filter kind is out of scope for the GPU path")
+    if estimate is None:
+        raise DimensionError(f"{kind} filter needs a covariance estimate")
+    device_mode = estimate._sp.device_mode if hasattr(estimate, "_sp") else nat.is_device(estimate.spatial)
+    sp = estimate._sp.dev() if hasattr(estimate, "_sp") else nat.to_device(estimate.spatial)
+    ua = subspace_basis_device(sp, estimate.rank_spatial, rank_tol)
+    tb = getattr(estimate, "_tb", None)
+    if tb is not None:
+        vecs, vals = tb
+        keep = 0
+        if vals[0] > 0.0:
+            while keep < min(estimate.rank_temporal, len(vals)) and vals[keep] > rank_tol * vals[0]:
+                keep += 1
+        ub = None if keep == 0 else vecs[:, :keep].contiguous()
+    else:
+        tp = estimate._tp.dev() if hasattr(estimate, "_tp") else nat.to_device(estimate.temporal)
+        ub = subspace_basis_device(tp, estimate.rank_temporal, rank_tol)
+    p_, q_ = sp.shape[0], (tb[0].shape[0] if tb is not None else
+                           (estimate._tp.dev().shape[0] if hasattr(estimate, "_tp")
+                            else np.shape(estimate.temporal)[0]))
+    f = StapFilter(kind, p_, q_,
+                   None if ua is None else Dual.from_device(ua, device_mode),
+                   None if ub is None else Dual.from_device(ub, device_mode),
+                   spatial_only=drop_temporal)
+    return f
+
+
+def make_doppler_grid(count):
+    """src/filters.py:201-205."""
+    if count < 1:
+        raise DimensionError(f"doppler grid needs at least one bin, got {count}")
+    return np.arange(count, dtype=np.float64) / count
+
+
+def make_spatial_grid(p, count=16):
+    """src/filters.py:208-217."""
+    if count < 1:
+        raise DimensionError(f"spatial grid needs at least one point, got {count}")
+    slopes = np.arange(count, dtype=np.float64) / count
+    return np.exp(2j * np.pi * np.outer(slopes, np.arange(p))) / np.sqrt(p)
+
+
+def make_stacked_spatial_grid(p, n_passes, count=16):
+    """src/filters.py:220-231."""
+    base = make_spatial_grid(p, count)
+    out = np.zeros((n_passes * count, n_passes * p), dtype=np.complex128)
+    for k in range(n_passes):
+        out[k * count:(k + 1) * count, k * p:(k + 1) * p] = base
+    return out
+
+
+@dataclass
+class DetectionMap:
+    """Per-bin, per-Doppler detection magnitudes with their grids (src/filters.py:234-240)."""
+
+    values: object
+    dopplers: np.ndarray
+    spatial_grid: np.ndarray
+
+
+def _host_grid_args(filt, dopplers, spatial_grid):
+    dop = np.ascontiguousarray(np.asarray(dopplers.cpu() if nat.is_device(dopplers) else dopplers,
+                                          dtype=np.float64).ravel())
+    grid = np.ascontiguousarray(np.asarray(spatial_grid.cpu() if nat.is_device(spatial_grid)
+                                           else spatial_grid, dtype=np.complex128))
+    if grid.ndim != 2 or grid.shape[1] != filt.p:
+        raise DimensionError(f"spatial grid shape {grid.shape} does not match p = {filt.p}")
+    return dop, grid
+
+
+def run_detect(filt, cube, dop, grid, groups=1):
+    """kst_detect -> device tensor (groups, n, D) float64."""
+    import torch
+    shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
+    if len(shp) != 3 or shp[1:] != (filt.p, filt.q):
+        raise DimensionError(f"cube shape {shp} does not match filter ({filt.p}, {filt.q})")
+    kind = filt._kind_code()
+    x = nat.to_device(cube)
+    ua, ub = filt._dev_bases()
+    n, D, G = shp[0], dop.size, grid.shape[0]
+    vals = torch.empty((groups, n, D), dtype=torch.float64, device=x.device)
+    c = nat.ctx(x.device)
+    nat.check(nat.lib().kst_detect(
+        c, nat.ptr(x), n, filt.p, filt.q, nat.ptr(ua), 0 if ua is None else ua.shape[1],
+        nat.ptr(ub), 0 if ub is None else ub.shape[1], kind, int(bool(filt.spatial_only)),
+        dop.ctypes.data_as(nat.C.c_void_p), D, grid.ctypes.data_as(nat.C.c_void_p), G, groups,
+        nat.ptr(vals), nat.stream_of(x.device)), c)
+    return vals
+
+
+def detection_image(filt, cube, dopplers, spatial_grid, pool=None):
+    """max_g |conj(H) F(X_m) conj(T)| per bin and Doppler (src/filters.py:243-275)."""
+    shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
+    if len(shp) != 3 or shp[1:] != (filt.p, filt.q):
+        raise DimensionError(f"cube shape {shp} does not match filter ({filt.p}, {filt.q})")
+    dop, grid = _host_grid_args(filt, dopplers, spatial_grid)
+    vals = run_detect(filt, cube, dop, grid)[0]
+    return DetectionMap(vals if nat.is_device(cube) else nat.to_host(vals), dop, grid)

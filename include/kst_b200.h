@@ -52,6 +52,15 @@ int kst_ctx_destroy(kst_ctx* ctx);
 const char* kst_last_error(const kst_ctx* ctx);
 int kst_version(void);
 
+/* Instrumentation (bench/profiling only; no effect on results):
+ * kst_launch_count: kernels launched by this context so far.
+ * kst_set_profiling(1): kst_pipeline records CUDA events at its stage
+ *   boundaries; kst_stage_times then returns up to `max` stage durations in
+ *   ms (scm, lrkron, bases, detect) of the last call, and the count. */
+long long kst_launch_count(const kst_ctx* ctx);
+int kst_set_profiling(kst_ctx* ctx, int on);
+int kst_stage_times(kst_ctx* ctx, double* ms, int max);
+
 /*
  * Sample covariance -- replaces `sample_covariance(snapshots, p, q)`
  * (src/lrkron.py:53-78): S = (1/n) X^T conj(X), exactly Hermitian.

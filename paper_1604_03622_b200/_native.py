@@ -28,6 +28,9 @@ _SIGS = {
     "kst_ctx_create": (_i, [_i, C.POINTER(_vp)]),
     "kst_ctx_destroy": (_i, [_vp]),
     "kst_last_error": (C.c_char_p, [_vp]),
+    "kst_launch_count": (C.c_longlong, [_vp]),
+    "kst_set_profiling": (_i, [_vp, _i]),
+    "kst_stage_times": (_i, [_vp, _vp, _i]),
     "kst_scm": (_i, [_vp, _vp, _i64, _i64, _vp, _vp]),
     "kst_lrkron": (_i, [_vp, _vp, _i, _i, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp, _vp, _ip, _ip,
                         _ip, _vp, _vp, _vp]),

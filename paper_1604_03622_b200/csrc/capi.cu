@@ -103,6 +103,8 @@ int kst_ctx_destroy(kst_ctx* ctx) {
     cudaDeviceSynchronize();
     for (auto& s : ctx->slots)
       if (s.ptr) cudaFree(s.ptr);
+    for (auto& e : ctx->ev)
+      if (e) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
   }
   delete ctx;
@@ -110,6 +112,30 @@ int kst_ctx_destroy(kst_ctx* ctx) {
 }
 
 const char* kst_last_error(const kst_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+long long kst_launch_count(const kst_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int kst_set_profiling(kst_ctx* ctx, int on) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  ctx->profiling = on;
+  ctx->n_ev = 0;
+  return KST_OK;
+}
+
+int kst_stage_times(kst_ctx* ctx, double* ms, int max) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  DeviceGuard g(ctx->device);
+  int k = 0;
+  for (; k + 1 < ctx->n_ev && k < max; ++k) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, ctx->ev[k], ctx->ev[k + 1]) != cudaSuccess) {
+      cudaGetLastError();
+      t = -1.f;
+    }
+    ms[k] = t;
+  }
+  return k;
+}
 
 int kst_scm(kst_ctx* ctx, const double* X, int64_t n, int64_t d, double* S, void* stream) {
   CTX_GUARD(ctx);
@@ -174,7 +200,9 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   cplx* spatial = (cplx*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 2 + 64);
   if (!S || !spatial) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
   cplx* ua = spatial + p * p;
+  stage_mark(ctx, 0, st);
   KST_TRY(kst::scm(ctx, (const cplx*)cube, n, d, S, st));
+  stage_mark(ctx, 1, st);
   // the temporal basis must survive until detection: dedicated slot
   const bool full_b = rank_temporal == q;
   cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal + 64);
@@ -185,6 +213,7 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   KST_TRY(kst::lrkron(ctx, S, p, q, rank_spatial, rank_temporal, tol, max_iter, 0, spatial,
                       temporal, full_b ? nullptr : ub, full_b ? nullptr : tbv.data(), &fit,
                       nullptr, nullptr, st));
+  stage_mark(ctx, 2, st);
   // build_filter (src/filters.py:164-175): U_A from the spatial factor
   int ka = 0, kb = 0;
   KST_TRY(kst::subspace_basis(ctx, spatial, p, rank_spatial, 1e-9, ua, &ka, st));
@@ -193,8 +222,10 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   } else if (tbv[0] > 0.0) {
     while (kb < rank_temporal && tbv[kb] > 1e-9 * tbv[0]) ++kb;
   }
+  stage_mark(ctx, 3, st);
   KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, ka ? ua : nullptr, ka, kb ? ub : nullptr, kb,
                       kind, 0, dopplers, D, (const cplx*)grid, G, groups, values, st));
+  stage_mark(ctx, 4, st);
   if (summary) {
     summary[0] = fit.iterations;
     summary[1] = fit.converged;

@@ -64,7 +64,21 @@ struct kst_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   void* cusolver = nullptr;  // cusolverDnHandle_t, created lazily (heig.cu fallback)
+  // instrumentation: kernel launches issued, and per-stage CUDA events of the
+  // last kst_pipeline call (recorded only when profiling is on)
+  long long launches = 0;
+  int profiling = 0;
+  cudaEvent_t ev[8] = {};
+  int n_ev = 0;
 };
+
+// record stage boundary k on `st` when profiling (kst_pipeline)
+inline void stage_mark(kst_ctx* ctx, int k, cudaStream_t st) {
+  if (!ctx->profiling || k >= 8) return;
+  if (!ctx->ev[k]) cudaEventCreate(&ctx->ev[k]);
+  cudaEventRecord(ctx->ev[k], st);
+  if (k + 1 > ctx->n_ev) ctx->n_ev = k + 1;
+}
 
 enum WsSlot {
   WS_S = 0,        // pq x pq covariance (pipeline)
@@ -83,7 +97,8 @@ enum WsSlot {
   WS_TMP = 13,      // short-lived copies
   WS_PIPE_UB = 14,  // pipeline: temporal basis (lives until detection)
   WS_PIPE_T = 15,   // pipeline: full temporal factor (rank_temporal == q only)
-  WS_PIPE_SP = 16   // pipeline: spatial factor + spatial basis
+  WS_PIPE_SP = 16,  // pipeline: spatial factor + spatial basis
+  WS_BZ = 17        // eigensolver: split-K partials of B*Z
 };
 
 void* ws_get(kst_ctx* ctx, int slot, size_t bytes);  // may return nullptr on OOM
@@ -101,6 +116,7 @@ int set_err(kst_ctx* ctx, int code, const char* fmt, ...);
 
 #define KST_LAUNCH(ctx)                                                                   \
   do {                                                                                    \
+    ++(ctx)->launches;                                                                    \
     cudaError_t e__ = cudaGetLastError();                                                 \
     if (e__ != cudaSuccess)                                                               \
       return set_err((ctx), KST_ERR_CUDA, "kernel launch failed: %s (%s:%d)",             \
@@ -146,6 +162,27 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   __syncthreads();
   return sh[0];
 }
+
+// Compile-time channel count dispatch (P = 1..16) for the per-channel kernels.
+#define KST_DISPATCH_P(P, CALL)                        \
+  switch (P) {                                         \
+    case 1: { constexpr int PP = 1; CALL; } break;     \
+    case 2: { constexpr int PP = 2; CALL; } break;     \
+    case 3: { constexpr int PP = 3; CALL; } break;     \
+    case 4: { constexpr int PP = 4; CALL; } break;     \
+    case 5: { constexpr int PP = 5; CALL; } break;     \
+    case 6: { constexpr int PP = 6; CALL; } break;     \
+    case 7: { constexpr int PP = 7; CALL; } break;     \
+    case 8: { constexpr int PP = 8; CALL; } break;     \
+    case 9: { constexpr int PP = 9; CALL; } break;     \
+    case 10: { constexpr int PP = 10; CALL; } break;   \
+    case 11: { constexpr int PP = 11; CALL; } break;   \
+    case 12: { constexpr int PP = 12; CALL; } break;   \
+    case 13: { constexpr int PP = 13; CALL; } break;   \
+    case 14: { constexpr int PP = 14; CALL; } break;   \
+    case 15: { constexpr int PP = 15; CALL; } break;   \
+    default: { constexpr int PP = 16; CALL; } break;   \
+  }
 
 // ---------------------------------------------------------------- internal API between units
 namespace kst {

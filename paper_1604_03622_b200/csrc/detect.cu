@@ -47,26 +47,92 @@ __global__ void twiddle_kernel(cplx* w, int D) {
   }
 }
 
-// In-place (ping-pong) Stockham DFT of length D over shared buffers.
-// Returns pointer to the buffer holding the result.
+// Ping-pong Stockham DFT (decimation in time) of length D over shared
+// buffers; w[k] = exp(-2 pi i k / D). Stage (radix R, Ns = product of the
+// previous radices, DR = D / R, step = D / (Ns R)), for j < DR, k = j mod Ns:
+//   t_r = a[j + r DR] * w[r k step],   X_u = sum_r t_r W_R^{ru},
+//   b[(j / Ns) Ns R + k + u Ns] = X_u.
+// Radix 2 and 4 use explicit butterflies. Odd radices pair outputs u, R-u:
+// with s_r = t_r + t_{R-r}, d_r = t_r - t_{R-r},
+//   X_u = t_0 + sum_r cos(2 pi r u / R) s_r -+ i sum_r sin(2 pi r u / R) d_r,
+// a quarter of the real multiply-adds of the direct R-point sum. All twiddle
+// indices are exact integers (no float phase accumulation).
+// Returns the buffer holding the result.
 __device__ cplx* stockham(cplx* a, cplx* b, const cplx* __restrict__ w, int D) {
   int Ns = 1;
+  const int nt = blockDim.x;
   for (int f = 0; f < c_plan.nf; ++f) {
     const int R = c_plan.radix[f];
     const int DR = D / R;
     const int step = D / (Ns * R);
-    for (int e = threadIdx.x; e < D; e += blockDim.x) {
-      const int j = e % DR, u = e / DR;
-      const int k = j % Ns;
-      const int base = (k + u * Ns) * step;  // exponent multiplier
-      cplx acc = cmk(0, 0);
-      int idx = 0;
-      for (int r = 0; r < R; ++r) {
-        cfma(acc, a[j + r * DR], w[idx]);
-        idx += base;
-        if (idx >= D) idx -= D * (idx / D);
+    if (R == 2 || R == 4) {
+      for (int j = threadIdx.x; j < DR; j += nt) {
+        const int k = j % Ns;
+        const int dst = (j / Ns) * Ns * R + k;
+        if (R == 2) {
+          const cplx t0 = a[j], t1 = cmul(a[j + DR], w[k * step]);
+          b[dst] = cadd(t0, t1);
+          b[dst + Ns] = csub(t0, t1);
+        } else {
+          const cplx t0 = a[j];
+          const cplx t1 = cmul(a[j + DR], w[k * step]);
+          const cplx t2 = cmul(a[j + 2 * DR], w[2 * k * step]);
+          const cplx t3 = cmul(a[j + 3 * DR], w[3 * k * step]);
+          const cplx s02 = cadd(t0, t2), d02 = csub(t0, t2);
+          const cplx s13 = cadd(t1, t3), d13 = csub(t1, t3);
+          // -i * d13 = (d13.y, -d13.x)
+          b[dst] = cadd(s02, s13);
+          b[dst + Ns] = cmk(d02.x + d13.y, d02.y - d13.x);
+          b[dst + 2 * Ns] = csub(s02, s13);
+          b[dst + 3 * Ns] = cmk(d02.x - d13.y, d02.y + d13.x);
+        }
       }
-      b[(j / Ns) * Ns * R + k + u * Ns] = acc;
+    } else {
+      const int h = (R - 1) / 2;
+      // phase A: stage twiddles, folded into (s_r, d_r) in place
+      for (int e = threadIdx.x; e < DR * h; e += nt) {
+        const int j = e % DR, r = 1 + e / DR;
+        const int k = j % Ns;
+        const cplx tr = cmul(a[j + r * DR], w[r * k * step]);
+        const cplx tm = cmul(a[j + (R - r) * DR], w[(R - r) * k * step]);
+        a[j + r * DR] = cadd(tr, tm);
+        a[j + (R - r) * DR] = csub(tr, tm);
+      }
+      __syncthreads();
+      // phase B: output pairs (u, R - u) and u = 0
+      const int DRR = D / R;  // W_R^m = w[m * D / R]
+      for (int e = threadIdx.x; e < DR * (h + 1); e += nt) {
+        const int j = e % DR, u = e / DR;
+        const int k = j % Ns;
+        const int dst = (j / Ns) * Ns * R + k;
+        const cplx t0 = a[j];
+        if (u == 0) {
+          cplx acc0 = t0, acc1 = cmk(0, 0);
+          int r = 1;
+          for (; r + 1 <= h; r += 2) {
+            acc0 = cadd(acc0, a[j + r * DR]);
+            acc1 = cadd(acc1, a[j + (r + 1) * DR]);
+          }
+          if (r <= h) acc0 = cadd(acc0, a[j + r * DR]);
+          b[dst] = cadd(acc0, acc1);
+        } else {
+          double ax = t0.x, ay = t0.y, bx = 0.0, by = 0.0;
+          int m = 0;
+          for (int r = 1; r <= h; ++r) {
+            m += u;
+            if (m >= R) m -= R;
+            const cplx wm = w[m * DRR];  // (cos, -sin)
+            const cplx sr = a[j + r * DR], dr = a[j + (R - r) * DR];
+            ax = fma(wm.x, sr.x, ax);
+            ay = fma(wm.x, sr.y, ay);
+            bx = fma(-wm.y, dr.x, bx);
+            by = fma(-wm.y, dr.y, by);
+          }
+          // X_u = A - iB, X_{R-u} = A + iB
+          b[dst + u * Ns] = cmk(ax + by, ay - bx);
+          b[dst + (R - u) * Ns] = cmk(ax - by, ay + bx);
+        }
+      }
     }
     __syncthreads();
     cplx* t = a;
@@ -87,21 +153,46 @@ __global__ void __launch_bounds__(NT) row_spectrum_kernel(
   __shared__ double red[32];
   const int64_t row = blockIdx.x;
   const cplx* x = src + row * q;
-  // 1. temporal coefficients c[k] = sum_t x[t] conj(ub[t, k])
+  // 1. temporal coefficients c[k] = sum_t x[t] conj(ub[t, k]), 4 at a time,
+  //    one fixed-order multi-value block reduction per group
   int bad = 0;
-  for (int k = 0; k < kb; ++k) {
-    double cr = 0.0, ci = 0.0;
+  __shared__ double red4[8][NT / 32];
+  for (int k0 = 0; k0 < kb; k0 += 4) {
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
     for (int t = threadIdx.x; t < q; t += NT) {
-      const cplx v = x[t], u = ub[(int64_t)t * kb + k];
-      cr = fma(v.x, u.x, cr);
-      cr = fma(v.y, u.y, cr);
-      ci = fma(v.y, u.x, ci);
-      ci = fma(-v.x, u.y, ci);
+      const cplx v = x[t];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < kb) {
+          const cplx w_ = ub[(int64_t)t * kb + k0 + u];
+          acc[2 * u] = fma(v.x, w_.x, acc[2 * u]);
+          acc[2 * u] = fma(v.y, w_.y, acc[2 * u]);
+          acc[2 * u + 1] = fma(v.y, w_.x, acc[2 * u + 1]);
+          acc[2 * u + 1] = fma(-v.x, w_.y, acc[2 * u + 1]);
+        }
+      }
     }
-    cr = block_sum<NT>(cr, red);
-    ci = block_sum<NT>(ci, red);
-    if (threadIdx.x == 0) coef[row * kb + k] = cmk(cr, ci);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = warp_sum(acc[u]);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) red4[u][wid] = acc[u];
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      double s_ = 0.0;
+      for (int w2 = 0; w2 < NT / 32; ++w2) s_ += red4[threadIdx.x][w2];
+      const int u = threadIdx.x >> 1;
+      if (k0 + u < kb) {
+        double* cp = (double*)&coef[row * kb + k0 + u];
+        cp[threadIdx.x & 1] = s_;
+      }
+    }
+    __syncthreads();
   }
+  (void)red;
   if (uniform) {
     cplx* a = smem;
     cplx* b = smem + D;
@@ -161,7 +252,9 @@ struct CombineArgs {
   double inv_sqrt_q;
 };
 
-// grid: (ceil(D / NT), n). One thread per Doppler.
+// grid: (ceil(D / NT), n). One thread per Doppler. Templated on the channel
+// count so the per-pixel channel loops are fully unrolled in registers.
+template <int PT>
 __global__ void __launch_bounds__(NT) combine_kernel(
     const cplx* __restrict__ spec, const cplx* __restrict__ coef, const cplx* __restrict__ ubspec,
     const cplx* __restrict__ ua, const cplx* __restrict__ hconj, CombineArgs a,
@@ -170,7 +263,7 @@ __global__ void __launch_bounds__(NT) combine_kernel(
   __shared__ cplx s_c[kMaxP * kMaxKB];
   extern __shared__ __align__(16) cplx s_h[];  // G x P conj grid
   const int64_t m = blockIdx.y;
-  const int P = a.P;
+  constexpr int P = PT;
   for (int e = threadIdx.x; e < P * a.ka; e += NT) s_ua[e] = ua[e];
   for (int e = threadIdx.x; e < a.G * P; e += NT) s_h[e] = hconj[e];
   if (a.mode != 2) {
@@ -224,16 +317,21 @@ __global__ void __launch_bounds__(NT) combine_kernel(
   }
   const int per = a.G / a.groups;
   for (int gr = 0; gr < a.groups; ++gr) {
-    double best = 0.0;
+    // max_g |z_g|: select by |z|^2, then one hypot (|.| as numpy computes it)
+    double best2 = -1.0;
+    cplx zb = cmk(0, 0);
     for (int g = gr * per; g < (gr + 1) * per; ++g) {
       cplx z = cmk(0, 0);
 #pragma unroll
       for (int i = 0; i < kMaxP; ++i)
         if (i < P) cfma(z, s_h[g * P + i], y[i]);
-      const double mag = hypot(z.x * a.inv_sqrt_q, z.y * a.inv_sqrt_q);
-      best = (g == gr * per) ? mag : fmax(best, mag);
+      const double m2 = cabs2(z);
+      if (m2 > best2) {
+        best2 = m2;
+        zb = z;
+      }
     }
-    values[((int64_t)gr * n + m) * a.D + d] = best;
+    values[((int64_t)gr * n + m) * a.D + d] = hypot(zb.x * a.inv_sqrt_q, zb.y * a.inv_sqrt_q);
   }
 }
 
@@ -451,8 +549,9 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   a.mode = mode;
   a.spatial = spatial;
   a.inv_sqrt_q = 1.0 / sqrt((double)q);
-  combine_kernel<<<dim3(cdiv(D, NT), (unsigned)n), NT, sizeof(cplx) * G * p, st>>>(
-      spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n);
+  KST_DISPATCH_P(p, (combine_kernel<PP><<<dim3(cdiv(D, NT), (unsigned)n), NT,
+                                          sizeof(cplx) * G * p, st>>>(
+                        spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n)));
   KST_LAUNCH(ctx);
   int hflag = 0;
   KST_CUDA(ctx, cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));

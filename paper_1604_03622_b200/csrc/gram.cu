@@ -1,41 +1,45 @@
-// K1: Hermitian sample-covariance Gram, FP64, for `sample_covariance`
-// (src/lrkron.py:53-78):  S = (1/n) X^T conj(X),  X = (n, d) snapshots.
+// K1: Hermitian sample-covariance Gram on the FP64 tensor cores, for
+// `sample_covariance` (src/lrkron.py:53-78):  S = (1/n) X^T conj(X),
+// X = (n, d) snapshots, d = p*q.
 //
 // Design:
-//  * Only upper-triangle 64x64 tiles are computed; each tile writes itself
-//    and its conjugate transpose, so S is exactly Hermitian (the reference
-//    symmetrises with (S + S^H)/2, src/lrkron.py:77) and the diagonal is real.
+//  * FP64 DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4): B200 runs FP64 at
+//    the same peak on the tensor pipe as on the DFMA pipe (measured 37 vs
+//    34 TFLOP/s, tools/fp64_peak), with 8x fewer issue slots per FMA.
 //  * 3M complex product: with planes xr, xi, s = xr + xi, d = xr - xi,
 //      Re = sum xr_a xr_b + xi_a xi_b,  Im = sum s_a d_b - xr_a xr_b + xi_a xi_b,
-//    i.e. three real FP64 FMAs per complex MAC instead of four.
-//  * Operand planes are produced once by gram_prep (zero-padded to the tile
-//    grid so the main loop has no bounds checks) and streamed into a
-//    3-stage cp.async shared-memory ring; 256 threads, 4x4 outputs each.
+//    three real GEMMs instead of four.
+//  * Only upper-triangle 64x64 tiles are computed; each writes itself and its
+//    conjugate transpose, so S is exactly Hermitian with a real diagonal (the
+//    reference symmetrises with (S + S^H)/2, src/lrkron.py:77).
+//  * Operand planes come from gram_prep (zero padded to the tile grid) and
+//    stream through a 4-stage cp.async ring; smem rows padded to 68 doubles
+//    so every fragment load is bank-conflict free. 8 warps, warp tile 32x16.
 #include "common.cuh"
 
 namespace {
 
-constexpr int BM = 64;          // tile edge (rows == cols)
-constexpr int BK = 8;           // snapshots per pipeline stage
-constexpr int STAGES = 3;
+constexpr int BM = 64;                  // tile edge (rows == cols)
+constexpr int BK = 8;                   // snapshots per pipeline stage
+constexpr int LD = BM + 4;              // padded smem row (doubles)
+constexpr int STAGES = 4;
 constexpr int NT = 256;
-constexpr int PLANE = BK * BM;  // doubles per plane per stage
+constexpr int PLANE = BK * LD;          // doubles per plane per stage
 constexpr int STAGE_DOUBLES = 6 * PLANE;  // A: xr, xi, s   B: xr, xi, d
 
 // planes[4][npad][dpad]: xr, xi, xr+xi, xr-xi
 __global__ void gram_prep(const cplx* __restrict__ X, int64_t n, int64_t d, int64_t npad,
                           int64_t dpad, double* __restrict__ planes) {
   const int64_t total = npad * dpad;
-  const int64_t plane = total;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = idx / dpad, a = idx - m * dpad;
     cplx v = cmk(0.0, 0.0);
     if (m < n && a < d) v = X[m * d + a];
     planes[idx] = v.x;
-    planes[plane + idx] = v.y;
-    planes[2 * plane + idx] = v.x + v.y;
-    planes[3 * plane + idx] = v.x - v.y;
+    planes[total + idx] = v.y;
+    planes[2 * total + idx] = v.x + v.y;
+    planes[3 * total + idx] = v.x - v.y;
   }
 }
 
@@ -49,6 +53,14 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// D(8x8) += A(8x4, row) * B(4x8, col); lane (g = lane/4, t = lane%4) holds
+// a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}.
+__device__ __forceinline__ void dmma(double2& c, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c.x), "+d"(c.y)
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ void tile_of(int t, int T, int& bi, int& bj) {
   // row-major enumeration of the upper triangle: row i holds T - i tiles
   double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * t;
@@ -60,55 +72,44 @@ __device__ __forceinline__ void tile_of(int t, int T, int& bi, int& bj) {
   bj = i + (t - (i * T - i * (i - 1) / 2));
 }
 
-__global__ void __launch_bounds__(NT, 1)
-gram_herm_3m(const double* __restrict__ planes, int64_t npad, int64_t dpad, int64_t n,
-             int64_t d, int T, cplx* __restrict__ S) {
+__global__ void __launch_bounds__(NT, 2)
+gram_herm_dmma(const double* __restrict__ planes, int64_t npad, int64_t dpad, int64_t n,
+               int64_t d, int T, cplx* __restrict__ S) {
   extern __shared__ __align__(16) double smem[];
   int bi, bj;
   tile_of(blockIdx.x, T, bi, bj);
   const int a0 = bi * BM, b0 = bj * BM;
   const int64_t plane = npad * dpad;
-  const double* gxr = planes;
-  const double* gxi = planes + plane;
-  const double* gs = planes + 2 * plane;
-  const double* gd = planes + 3 * plane;
-
   const int tid = threadIdx.x;
-  // loader mapping: each stage moves 6 planes x BK rows x 64 doubles = 1536
-  // 16-byte chunks; thread handles chunks tid + 256*c, c < 6.
+
+  // loader: 6 planes x BK rows x 32 chunks(16 B) = 1536 chunks, 6 per thread
   auto load_stage = [&](int stage, int kb) {
     double* base = smem + stage * STAGE_DOUBLES;
     const int64_t m0 = (int64_t)kb * BK;
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
-      const int chunk = tid + NT * c;      // 0..1535
-      const int pl = chunk >> 8;           // 256 chunks per plane
+      const int chunk = tid + NT * c;
+      const int pl = chunk >> 8;
       const int within = chunk & 255;
-      const int row = within >> 5;         // 32 chunks per row (64 doubles)
+      const int row = within >> 5;
       const int col = (within & 31) * 2;
-      const double* src;
-      int colbase;
-      switch (pl) {
-        case 0: src = gxr; colbase = a0; break;
-        case 1: src = gxi; colbase = a0; break;
-        case 2: src = gs; colbase = a0; break;
-        case 3: src = gxr; colbase = b0; break;
-        case 4: src = gxi; colbase = b0; break;
-        default: src = gd; colbase = b0; break;
-      }
-      cp_async16(base + pl * PLANE + row * BM + col, src + (m0 + row) * dpad + colbase + col);
+      const int src_plane = pl < 3 ? pl : (pl == 5 ? 3 : pl - 3);  // A: xr xi s  B: xr xi d
+      const int colbase = pl < 3 ? a0 : b0;
+      cp_async16(base + pl * PLANE + row * LD + col,
+                 planes + src_plane * plane + (m0 + row) * dpad + colbase + col);
     }
   };
 
   const int w = tid >> 5, lane = tid & 31;
-  const int r0 = (w >> 1) * 16 + (lane >> 3) * 4;  // 4 contiguous rows
-  const int c0 = (w & 1) * 32 + (lane & 7) * 4;    // 4 contiguous cols
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (w >> 2) * 32;  // warp tile rows  [wr, wr+32)
+  const int wc = (w & 3) * 16;   // warp tile cols  [wc, wc+16)
 
-  double t1[4][4], t2[4][4], t3[4][4];
+  double2 t1[4][2], t2[4][2], t3[4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) t1[i][j] = t2[i][j] = t3[i][j] = 0.0;
+    for (int j = 0; j < 2; ++j) t1[i][j] = t2[i][j] = t3[i][j] = make_double2(0.0, 0.0);
 
   const int nk = (int)(npad / BK);
 #pragma unroll
@@ -126,33 +127,30 @@ gram_herm_3m(const double* __restrict__ planes, int64_t npad, int64_t dpad, int6
     }
     const double* st = smem + (kb % STAGES) * STAGE_DOUBLES;
 #pragma unroll
-    for (int k = 0; k < BK; ++k) {
-      const double* ar = st + 0 * PLANE + k * BM + r0;
-      const double* ai = st + 1 * PLANE + k * BM + r0;
-      const double* as = st + 2 * PLANE + k * BM + r0;
-      const double* br = st + 3 * PLANE + k * BM + c0;
-      const double* bi_ = st + 4 * PLANE + k * BM + c0;
-      const double* bd = st + 5 * PLANE + k * BM + c0;
-      double xr[4], xi[4], xs[4], yr[4], yi[4], yd[4];
-      *(double2*)&xr[0] = *(const double2*)&ar[0];
-      *(double2*)&xr[2] = *(const double2*)&ar[2];
-      *(double2*)&xi[0] = *(const double2*)&ai[0];
-      *(double2*)&xi[2] = *(const double2*)&ai[2];
-      *(double2*)&xs[0] = *(const double2*)&as[0];
-      *(double2*)&xs[2] = *(const double2*)&as[2];
-      *(double2*)&yr[0] = *(const double2*)&br[0];
-      *(double2*)&yr[2] = *(const double2*)&br[2];
-      *(double2*)&yi[0] = *(const double2*)&bi_[0];
-      *(double2*)&yi[2] = *(const double2*)&bi_[2];
-      *(double2*)&yd[0] = *(const double2*)&bd[0];
-      *(double2*)&yd[2] = *(const double2*)&bd[2];
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int ro = (kk + t) * LD;
+      double xr[4], xi[4], xs[4], yr[2], yi[2], yd[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int a = ro + wr + 8 * i + g;
+        xr[i] = st[0 * PLANE + a];
+        xi[i] = st[1 * PLANE + a];
+        xs[i] = st[2 * PLANE + a];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int b = ro + wc + 8 * j + g;
+        yr[j] = st[3 * PLANE + b];
+        yi[j] = st[4 * PLANE + b];
+        yd[j] = st[5 * PLANE + b];
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          t1[i][j] = fma(xr[i], yr[j], t1[i][j]);
-          t2[i][j] = fma(xi[i], yi[j], t2[i][j]);
-          t3[i][j] = fma(xs[i], yd[j], t3[i][j]);
+        for (int j = 0; j < 2; ++j) {
+          dmma(t1[i][j], xr[i], yr[j]);
+          dmma(t2[i][j], xi[i], yi[j]);
+          dmma(t3[i][j], xs[i], yd[j]);
         }
     }
   }
@@ -161,18 +159,24 @@ gram_herm_3m(const double* __restrict__ planes, int64_t npad, int64_t dpad, int6
   const double dn = (double)n;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int a = a0 + r0 + i;
+    const int a = a0 + wr + 8 * i + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int b = b0 + c0 + j;
-      if (a >= d || b >= d) continue;
-      const double re = (t1[i][j] + t2[i][j]) / dn;
-      const double im = (t3[i][j] - t1[i][j] + t2[i][j]) / dn;
-      if (bi != bj || a < b) {
-        S[(int64_t)a * d + b] = cmk(re, im);
-        S[(int64_t)b * d + a] = cmk(re, -im);
-      } else if (a == b) {
-        S[(int64_t)a * d + a] = cmk(re, 0.0);
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = b0 + wc + 8 * j + 2 * t + e;
+        if (a >= d || b >= d) continue;
+        const double v1 = e ? t1[i][j].y : t1[i][j].x;
+        const double v2 = e ? t2[i][j].y : t2[i][j].x;
+        const double v3 = e ? t3[i][j].y : t3[i][j].x;
+        const double re = (v1 + v2) / dn;
+        const double im = (v3 - v1 + v2) / dn;
+        if (bi != bj || a < b) {
+          S[(int64_t)a * d + b] = cmk(re, im);
+          S[(int64_t)b * d + a] = cmk(re, -im);
+        } else if (a == b) {
+          S[(int64_t)a * d + a] = cmk(re, 0.0);
+        }
       }
     }
   }
@@ -199,11 +203,11 @@ int scm(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, cudaStream_t
   const size_t smem = sizeof(double) * STAGES * STAGE_DOUBLES;
   static bool attr = false;
   if (!attr) {
-    KST_CUDA(ctx, cudaFuncSetAttribute(gram_herm_3m, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KST_CUDA(ctx, cudaFuncSetAttribute(gram_herm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     attr = true;
   }
-  gram_herm_3m<<<tiles, NT, smem, st>>>(planes, npad, dpad, n, d, T, S);
+  gram_herm_dmma<<<tiles, NT, smem, st>>>(planes, npad, dpad, n, d, T, S);
   KST_LAUNCH(ctx);
   return KST_OK;
 }

@@ -38,42 +38,51 @@ __global__ void jacobi_eig_kernel(const cplx* __restrict__ M, int ldm, int n, do
 }
 
 // ---------------------------------------------------------------- tall-skinny kernels
-// Y (n x s) = B (n x n) * Z (n x s); s <= 32, multiple of 8. 128 threads,
-// 16 rows per CTA, K staged through shared memory in chunks of 32.
-constexpr int BZ_ROWS = 16, BZ_K = 32;
+// Ypart[ks] (n x s) = B[:, kslice] * Z[kslice, :]; s <= 32. Split-K over
+// blockIdx.y (BZ_KSPLIT columns of B each) so ~1000 CTAs stream the 64 MB
+// matrix; the partials are summed in a fixed order afterwards.
+constexpr int BZ_ROWS = 16, BZ_K = 32, BZ_KSPLIT = 256;
 __global__ void __launch_bounds__(128) bz_kernel(const cplx* __restrict__ B, int n,
                                                  const cplx* __restrict__ Z, int s,
-                                                 cplx* __restrict__ Y) {
+                                                 cplx* __restrict__ Ypart) {
   __shared__ cplx sb[BZ_ROWS][BZ_K + 1];
   __shared__ cplx sz[BZ_K][32 + 1];
   const int r0 = blockIdx.x * BZ_ROWS;
+  const int kbeg = blockIdx.y * BZ_KSPLIT, kend = min(n, kbeg + BZ_KSPLIT);
   const int t = threadIdx.x;
   const int row = t >> 3, cg = t & 7;  // 16 rows x 8 column groups
   cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-  for (int k0 = 0; k0 < n; k0 += BZ_K) {
+  for (int k0 = kbeg; k0 < kend; k0 += BZ_K) {
     for (int e = t; e < BZ_ROWS * BZ_K; e += 128) {
       const int rr = e / BZ_K, kk = e % BZ_K;
       const int gr = r0 + rr, gk = k0 + kk;
-      sb[rr][kk] = (gr < n && gk < n) ? B[(size_t)gr * n + gk] : cmk(0, 0);
+      sb[rr][kk] = (gr < n && gk < kend) ? B[(size_t)gr * n + gk] : cmk(0, 0);
     }
     for (int e = t; e < BZ_K * s; e += 128) {
       const int kk = e / s, c = e % s;
       const int gk = k0 + kk;
-      sz[kk][c] = gk < n ? Z[(size_t)gk * s + c] : cmk(0, 0);
+      sz[kk][c] = gk < kend ? Z[(size_t)gk * s + c] : cmk(0, 0);
     }
     __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < BZ_K; ++kk) {
-      const cplx b = sb[row][kk];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int col = cg + 8 * c;
-        if (col < s) cfma(acc[c], b, sz[kk][col]);
-      }
+    // only the column groups this thread owns (no predicated-off DFMAs)
+    const int ncol = (s - cg + 7) >> 3;
+#define BZ_CASE(NC)                                                      \
+  for (int kk = 0; kk < BZ_K; ++kk) {                                    \
+    const cplx b = sb[row][kk];                                          \
+    _Pragma("unroll") for (int c = 0; c < NC; ++c) cfma(acc[c], b, sz[kk][cg + 8 * c]); \
+  }
+    switch (ncol) {
+      case 1: BZ_CASE(1) break;
+      case 2: BZ_CASE(2) break;
+      case 3: BZ_CASE(3) break;
+      case 4: BZ_CASE(4) break;
+      default: break;
     }
+#undef BZ_CASE
     __syncthreads();
   }
   const int gr = r0 + row;
+  cplx* Y = Ypart + (size_t)blockIdx.y * n * s;
   if (gr < n) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -342,6 +351,256 @@ unsigned grid_for(int64_t total, int nt = 256) {
 }
 
 // ---------------------------------------------------------------- host helpers
+// ---------------------------------------------------------------- K4 v2 kernels
+// Block power iteration with Rayleigh-Ritz and scaled-SVQB orthonormalisation:
+//   Y = B Z;  H = Z^H Y = Q Theta Q^H (Ritz);  G' = (YQ)^H (YQ);
+//   D = diag(G')^-1/2;  D G' D = V S^2 V^H;  Z <- Y Q D V S^-1.
+// Ritz residuals |Y q_k - theta_k Z q_k| are formed directly (no Gram
+// cancellation). All small-matrix work runs in one CTA (k4_small_kernel).
+constexpr int K4_ROWS = 16;
+
+// partial[blk] = {Z^H Y1, Y2^H Y2} over a chunk of rows (s x s each)
+__global__ void __launch_bounds__(256) k4_gram_kernel(const cplx* __restrict__ Z,
+                                                      const cplx* __restrict__ Y1,
+                                                      const cplx* __restrict__ Y2, int n, int s,
+                                                      cplx* __restrict__ partial) {
+  __shared__ cplx sz[K4_ROWS][33];
+  __shared__ cplx sy[K4_ROWS][33];
+  __shared__ cplx s2[K4_ROWS][33];
+  // each CTA walks row tiles blockIdx.x, +gridDim.x, ... (few partials to reduce)
+  cplx acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = cmk(0, 0);
+  for (int r0 = blockIdx.x * K4_ROWS; r0 < n; r0 += gridDim.x * K4_ROWS) {
+    const int rows = min(K4_ROWS, n - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < K4_ROWS * s; e += 256) {
+      const int rr = e / s, a = e % s;
+      sz[rr][a] = rr < rows ? Z[(size_t)(r0 + rr) * s + a] : cmk(0, 0);
+      sy[rr][a] = rr < rows ? Y1[(size_t)(r0 + rr) * s + a] : cmk(0, 0);
+      s2[rr][a] = rr < rows ? Y2[(size_t)(r0 + rr) * s + a] : cmk(0, 0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      if (e < 2 * s * s) {
+        const int which = e / (s * s), ab = e % (s * s);
+        const int a = ab / s, b = ab % s;
+        if (which == 0)
+          for (int rr = 0; rr < K4_ROWS; ++rr) cfmca(acc[u], sz[rr][a], sy[rr][b]);
+        else
+          for (int rr = 0; rr < K4_ROWS; ++rr) cfmca(acc[u], s2[rr][a], s2[rr][b]);
+      }
+    }
+  }
+  cplx* out = partial + (size_t)blockIdx.x * 2 * s * s;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + 256 * u;
+    if (e < 2 * s * s) out[e] = acc[u];
+  }
+}
+
+// One CTA. mode 0: Rayleigh-Ritz + orthonormalise Y; mode 1: orthonormalise
+// only (Q = I). Writes C (s x s), Q (s x s), theta (s), info[0] = kept columns,
+// info[1] = Jacobi sweeps (diagnostic).
+__global__ void __launch_bounds__(256) k4_small_kernel(const cplx* __restrict__ partial, int nblk,
+                                                       int s, int mode, cplx* __restrict__ Cout,
+                                                       cplx* __restrict__ Qout,
+                                                       double* __restrict__ theta,
+                                                       int* __restrict__ info) {
+  extern __shared__ __align__(16) char sm[];
+  __shared__ double dsc[32], th[32];
+  cplx* H = (cplx*)(sm + ((jac_smem_bytes(s) + 15) / 16) * 16);
+  cplx* G = H + s * s;
+  cplx* Q = G + s * s;
+  cplx* T = Q + s * s;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  const int nw = blockDim.x >> 5;
+  // fixed-order reduction of the partials
+  for (int k = w; k < 4 * s * s; k += nw) {
+    const int comp = k & 1, e = k >> 1;  // e indexes [which][a][b]
+    double acc = 0.0;
+    for (int b = l; b < nblk; b += 32) {
+      const cplx v = partial[(size_t)b * 2 * s * s + e];
+      acc += comp ? v.y : v.x;
+    }
+    acc = warp_sum(acc);
+    if (l == 0) {
+      cplx* dst = e < s * s ? &H[e] : &G[e - s * s];
+      if (comp) dst->y = acc;
+      else dst->x = acc;
+    }
+  }
+  __syncthreads();
+  JacSmem j = jac_carve(sm, s);
+  if (mode == 0) {
+    jac_load_sym(j, H, s, s, 1.0);
+    jac_sweeps(j, s);
+    jac_finish(j, s);
+    for (int e = tid; e < s * s; e += blockDim.x) {
+      const int i = e / s, k = e % s;
+      Q[e] = j.V[i * j.ld + j.order[k]];
+    }
+    for (int k = tid; k < s; k += blockDim.x) th[k] = j.val[j.order[k]];
+  } else {
+    for (int e = tid; e < s * s; e += 256) Q[e] = cmk((e / s) == (e % s) ? 1.0 : 0.0, 0.0);
+    for (int k = tid; k < s; k += blockDim.x) th[k] = 0.0;
+  }
+  __syncthreads();
+  // T = G Q, then G' = Q^H T (reuse H)
+  for (int e = tid; e < s * s; e += blockDim.x) {
+    const int a = e / s, k = e % s;
+    cplx acc = cmk(0, 0);
+    for (int b = 0; b < s; ++b) cfma(acc, G[a * s + b], Q[b * s + k]);
+    T[e] = acc;
+  }
+  __syncthreads();
+  for (int e = tid; e < s * s; e += blockDim.x) {
+    const int a = e / s, k = e % s;
+    cplx acc = cmk(0, 0);
+    for (int b = 0; b < s; ++b) cfmca(acc, Q[b * s + a], T[b * s + k]);
+    H[e] = acc;
+  }
+  __syncthreads();
+  for (int k = tid; k < s; k += blockDim.x) {
+    const double g = H[k * s + k].x;
+    dsc[k] = g > 0.0 ? 1.0 / sqrt(g) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < s * s; e += blockDim.x) {
+    const int a = e / s, b = e % s;
+    G[e] = cscale(H[e], dsc[a] * dsc[b]);
+  }
+  __syncthreads();
+  // Fast path: scaled Cholesky QR. G~ = R^H R (R upper, in T), C = Q D R^-1.
+  // Taken when every pivot stays >= 1e-10 (well-conditioned block, i.e. all
+  // iterations after the first); otherwise fall through to SVQB by Jacobi.
+  {
+    __shared__ int chol_ok;
+    for (int e = tid; e < s * s; e += blockDim.x) T[e] = G[e];
+    if (tid == 0) chol_ok = 1;
+    __syncthreads();
+    for (int k = 0; k < s; ++k) {
+      const double dkk = T[k * s + k].x;
+      if (!(dkk >= 1e-10)) {
+        if (tid == 0) chol_ok = 0;
+        break;  // uniform across the block (all threads read the same dkk)
+      }
+      const double rkk = sqrt(dkk);
+      __syncthreads();
+      // row k of R: R[k][j] = T[k][j] / rkk (j > k); R[k][k] = rkk
+      for (int jj = k + 1 + tid; jj < s; jj += blockDim.x) T[k * s + jj] = cscale(T[k * s + jj], 1.0 / rkk);
+      __syncthreads();
+      if (tid == 0) T[k * s + k] = cmk(rkk, 0.0);
+      // trailing update T[i][jj] -= conj(R[k][i]) R[k][jj], i, jj > k
+      const int m = s - k - 1;
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int i = k + 1 + e / m, jj = k + 1 + e % m;
+        const cplx a = T[k * s + i], b = T[k * s + jj];
+        T[i * s + jj] = csub(T[i * s + jj], cmk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x));
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (chol_ok) {
+      // Rinv (upper) by column-parallel back substitution, stored in G
+      for (int col = tid; col < s; col += blockDim.x) {
+        for (int i = s - 1; i >= 0; --i) {
+          cplx acc = cmk(i == col ? 1.0 : 0.0, 0.0);
+          for (int jj = i + 1; jj <= col; ++jj) acc = csub(acc, cmul(T[i * s + jj], G[jj * s + col]));
+          G[i * s + col] = i > col ? cmk(0, 0) : cscale(acc, 1.0 / T[i * s + i].x);
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < s * s; e += blockDim.x) {
+        const int a = e / s, k = e % s;
+        cplx acc = cmk(0, 0);
+        for (int b = 0; b <= k; ++b) cfma(acc, Q[a * s + b], cscale(G[b * s + k], dsc[b]));
+        Cout[e] = acc;
+        Qout[e] = Q[e];
+      }
+      if (tid == 0) {
+        info[0] = s;
+        info[1] = 2;  // Cholesky path
+      }
+      if (mode == 0)
+        for (int k = tid; k < s; k += blockDim.x) theta[k] = th[k];
+      return;
+    }
+  }
+  jac_load_sym(j, G, s, s, 1.0);
+  jac_sweeps(j, s);
+  jac_finish(j, s);
+  // C = Q D V S^-1. Nearly dependent directions are NOT dropped: their tiny
+  // singular values are floored, so they come back as amplified rounding
+  // noise -- fresh trial directions -- and the next pass orthonormalises them.
+  const double smax = j.val[j.order[0]];
+  for (int e = tid; e < s * s; e += blockDim.x) {
+    const int a = e / s, k = e % s;
+    const double sg = fmax(j.val[j.order[k]], 1e-30 * smax);
+    cplx acc = cmk(0, 0);
+    if (smax > 0.0) {
+      const double inv = 1.0 / sqrt(sg);
+      for (int b = 0; b < s; ++b)
+        cfma(acc, Q[a * s + b], cscale(j.V[b * j.ld + j.order[k]], dsc[b] * inv));
+    }
+    Cout[e] = acc;
+    Qout[e] = Q[e];
+  }
+  if (tid == 0) {
+    int kept = 0;
+    for (int k = 0; k < s; ++k) kept += (smax > 0.0 && j.val[j.order[k]] > 1e-26 * smax) ? 1 : 0;
+    info[0] = kept;  // diagnostic: numerically independent directions
+    info[1] = smax > 0.0 ? 1 : 0;
+  }
+  if (mode == 0)
+    for (int k = tid; k < s; k += blockDim.x) theta[k] = th[k];
+}
+
+// Z_new = Y C; X = Z Q (Ritz vectors); residual partials sum_rows |Y q_k - th_k X_k|^2
+// blockDim (32, 8): x = column, y = row in block. mode 1: only Z_new = Y C.
+__global__ void __launch_bounds__(256) k4_update_kernel(
+    const cplx* __restrict__ Y, const cplx* __restrict__ Y2, const cplx* __restrict__ Z, int n,
+    int s, int r, int mode,
+    const cplx* __restrict__ C, const cplx* __restrict__ Q, const double* __restrict__ theta,
+    cplx* __restrict__ Znew, cplx* __restrict__ X, double* __restrict__ res_part) {
+  __shared__ cplx sC[32 * 32], sQ[32 * 32];
+  __shared__ double sres[8][32];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int e = tid; e < s * s; e += 256) {
+    sC[e] = C[e];
+    sQ[e] = Q[e];
+  }
+  __syncthreads();
+  const int row = blockIdx.x * 8 + threadIdx.y, k = threadIdx.x;
+  double rr = 0.0;
+  if (row < n && k < s) {
+    cplx zn = cmk(0, 0), x = cmk(0, 0), yq = cmk(0, 0);
+    for (int a = 0; a < s; ++a) {
+      const cplx y = Y[(size_t)row * s + a];
+      cfma(zn, Y2[(size_t)row * s + a], sC[a * s + k]);
+      if (mode == 0) {
+        cfma(yq, y, sQ[a * s + k]);
+        cfma(x, Z[(size_t)row * s + a], sQ[a * s + k]);
+      }
+    }
+    Znew[(size_t)row * s + k] = zn;
+    if (mode == 0) {
+      X[(size_t)row * s + k] = x;
+      if (k < r) rr = cabs2(cmk(yq.x - theta[k] * x.x, yq.y - theta[k] * x.y));
+    }
+  }
+  sres[threadIdx.y][threadIdx.x] = rr;
+  __syncthreads();
+  if (mode == 0 && threadIdx.y == 0 && k < r) {
+    double acc = 0.0;
+    for (int i = 0; i < 8; ++i) acc += sres[i][k];
+    res_part[(size_t)blockIdx.x * r + k] = acc;
+  }
+}
+
 struct TsCtx {
   kst_ctx* ctx;
   cudaStream_t st;
@@ -371,6 +630,17 @@ int ts_mul(TsCtx& t, const cplx* U, int ldu, int s1, const cplx* C, int ldc, int
   ts_mul_kernel<<<grid_for((int64_t)n * s2), 256, sizeof(cplx) * s1 * s2, t.st>>>(
       U, ldu, s1, C, ldc, s2, X0, ldx, Out, ldo, n);
   KST_LAUNCH(t.ctx);
+  return KST_OK;
+}
+
+int bz(kst_ctx* ctx, const cplx* B, int n, const cplx* Z, int s, cplx* Y, cudaStream_t st) {
+  const int ks = (n + BZ_KSPLIT - 1) / BZ_KSPLIT;
+  cplx* part = (cplx*)ws_get(ctx, WS_BZ, sizeof(cplx) * (size_t)ks * n * s);
+  if (!part) return set_err(ctx, KST_ERR_CUDA, "bz: workspace");
+  bz_kernel<<<dim3(cdiv(n, BZ_ROWS), ks), 128, 0, st>>>(B, n, Z, s, part);
+  KST_LAUNCH(ctx);
+  reduce_partials_kernel<<<grid_for((int64_t)n * s), 256, 0, st>>>(part, ks, n * s, Y);
+  KST_LAUNCH(ctx);
   return KST_OK;
 }
 
@@ -516,123 +786,101 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   }
   if (r > 24) return heig_top_cusolver(ctx, M, n, r, values_host, vectors, st);
 
-  int s = std::max(r + 6, 8);
-  s = ((s + 7) / 8) * 8;
-  if (s > 32) s = 32;
-  const int s2 = 2 * s;
-  // workspace layout
+  // block: r wanted + >= 5 guard vectors (convergence rate lambda_{s+1}/lambda_r)
+  const int s = std::min(32, std::max(8, r + 5));
   const size_t nb = (size_t)n * s;
-  size_t bytes = sizeof(cplx) * (nb * 8 + (size_t)s2 * s2 * 3 + (size_t)s * s * 4) +
-                 sizeof(double) * (s2 * 2 + s * 4) + sizeof(int) * (s + 8) + 256;
+  const int nblk = std::min((n + K4_ROWS - 1) / K4_ROWS, 32);
+  const int nup = (n + 7) / 8;
+  size_t bytes = sizeof(cplx) * (nb * 5 + (size_t)s * s * 2) + sizeof(double) * (2 * s) +
+                 sizeof(int) * 8 + 256;
   char* base = (char*)ws_get(ctx, WS_EIG, bytes);
-  const int nblk = (n + GP_ROWS - 1) / GP_ROWS;
-  cplx* partial = (cplx*)ws_get(ctx, WS_EIG2, sizeof(cplx) * (size_t)nblk * s2 * s2);
-  double* hres = (double*)pinned_get(ctx, sizeof(double) * 2 * s2);
+  cplx* partial = (cplx*)ws_get(ctx, WS_EIG2, sizeof(cplx) * (size_t)nblk * 2 * s * s +
+                                                  sizeof(double) * (size_t)nup * r + 64);
+  double* hres = (double*)pinned_get(ctx, sizeof(double) * ((size_t)nup * r + s + 8));
   if (!base || !partial || !hres) return set_err(ctx, KST_ERR_CUDA, "heig_top: workspace");
-  cplx* Vb = (cplx*)base;    // [Z | W]   n x 2s
-  cplx* Tb = Vb + 2 * nb;    // [Y | BW]  n x 2s
-  cplx* Zn = Tb + 2 * nb;    // new Z     n x s
-  cplx* Yn = Zn + nb;        // new Y     n x s
-  cplx* Wt = Yn + nb;        // temp      n x s
-  cplx* Wt2 = Wt + nb;       // temp2     n x s
-  cplx* H = Wt2 + nb;        // s2 x s2
-  cplx* Hv = H + s2 * s2;    // s2 x s2 eigenvectors
-  cplx* Cs = Hv + s2 * s2;   // s x s coefficients
-  cplx* Gs = Cs + s * s;     // s x s gram
-  cplx* Gv = Gs + s * s;     // s x s eigvecs
-  cplx* Cs2 = Gv + s * s;    // s x s
-  double* Hval = (double*)(Cs2 + s * s);
-  double* Gval = Hval + s2;
-  double* theta = Gval + s2;
-  double* res = theta + s;
-  double* vout = res + s;
-  int* mask = (int*)(vout + s);
-  TsCtx t{ctx, st, partial};
-
-  // Z stored at ld 2s inside Vb (columns 0..s-1), W at columns s..2s-1
-  const int ldV = s2;
-  // Orthonormalise a block X (n x s, ld ldx) in place via two SVQB passes,
-  // optionally against Z first. Returns via mask which columns survived.
-  auto svqb = [&](cplx* X, int ldx, bool against_z, int* msk) -> int {
-    for (int pass = 0; pass < 2; ++pass) {
-      if (against_z) {
-        // X -= Z (Z^H X)
-        KST_TRY(gram_ts(t, Vb, ldV, s, X, ldx, s, n, Cs));
-        KST_TRY(ts_mul(t, Vb, ldV, s, Cs, s, s, X, ldx, Wt, s, n));
-        KST_CUDA(ctx, cudaMemcpy2DAsync(X, sizeof(cplx) * ldx, Wt, sizeof(cplx) * s,
-                                        sizeof(cplx) * s, n, cudaMemcpyDeviceToDevice, st));
-      }
-      KST_TRY(gram_ts(t, X, ldx, s, X, ldx, s, n, Gs));
-      KST_TRY(jacobi(ctx, Gs, s, s, 1.0, Gval, Gv, s, st));
-      svqb_coeff_kernel<<<1, 256, 0, st>>>(Gval, Gv, s, 1e-24, Cs2, pass == 1 ? msk : nullptr);
-      KST_LAUNCH(ctx);
-      KST_TRY(ts_mul(t, X, ldx, s, Cs2, s, s, nullptr, 0, Wt2, s, n));
-      KST_CUDA(ctx, cudaMemcpy2DAsync(X, sizeof(cplx) * ldx, Wt2, sizeof(cplx) * s,
-                                      sizeof(cplx) * s, n, cudaMemcpyDeviceToDevice, st));
-    }
+  cplx* Z = (cplx*)base;
+  cplx* Y = Z + nb;
+  cplx* Y2 = Y + nb;
+  cplx* Zn = Y2 + nb;
+  cplx* X = Zn + nb;
+  cplx* Cm = X + nb;
+  cplx* Qm = Cm + s * s;
+  double* theta = (double*)(Qm + s * s);
+  double* vout = theta + s;
+  int* info = (int*)(vout + s);
+  double* res_part = (double*)(partial + (size_t)nblk * 2 * s * s);
+  const size_t small_smem = ((jac_smem_bytes(s) + 15) / 16) * 16 + sizeof(cplx) * 4 * s * s;
+  static bool small_attr = false;
+  if (!small_attr) {
+    KST_CUDA(ctx, cudaFuncSetAttribute(k4_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(((jac_smem_bytes(32) + 15) / 16) * 16 +
+                                             sizeof(cplx) * 4 * 32 * 32)));
+    small_attr = true;
+  }
+  // mode 0: Ritz pairs of span(Zc) from Y1 = B Zc; next block = orth(Y2), Y2 = B Y1
+  // mode 1: Zc <- orth(Y2) only
+  auto step = [&](const cplx* Zc, const cplx* Y1, const cplx* Y2c, int mode) -> int {
+    k4_gram_kernel<<<nblk, 256, 0, st>>>(Zc, Y1, Y2c, n, s, partial);
+    KST_LAUNCH(ctx);
+    k4_small_kernel<<<1, 64, small_smem, st>>>(partial, nblk, s, mode, Cm, Qm, theta, info);
+    KST_LAUNCH(ctx);
+    k4_update_kernel<<<nup, dim3(32, 8), 0, st>>>(Y1, Y2c, Zc, n, s, r, mode, Cm, Qm, theta, Zn,
+                                                   X, res_part);
+    KST_LAUNCH(ctx);
+    std::swap(Z, Zn);  // Zn (= Y2 C) becomes the current block
     return KST_OK;
   };
-
-  // Z0 = orth(random); Y0 = B Z0
-  random_block_kernel<<<grid_for((int64_t)n * s), 256, 0, st>>>(Wt, n, s, 0x5EEDull + n);
+  // Z0 = orth(random), two orthonormalisation passes
+  random_block_kernel<<<grid_for((int64_t)n * s), 256, 0, st>>>(Z, n, s, 0x5EEDull + n);
   KST_LAUNCH(ctx);
-  KST_CUDA(ctx, cudaMemcpy2DAsync(Vb, sizeof(cplx) * ldV, Wt, sizeof(cplx) * s, sizeof(cplx) * s,
-                                  n, cudaMemcpyDeviceToDevice, st));
-  KST_TRY(svqb(Vb, ldV, false, mask));
-  KST_CUDA(ctx, cudaMemcpy2DAsync(Zn, sizeof(cplx) * s, Vb, sizeof(cplx) * ldV, sizeof(cplx) * s,
-                                  n, cudaMemcpyDeviceToDevice, st));
-  bz_kernel<<<cdiv(n, BZ_ROWS), 128, 0, st>>>(M, n, Zn, s, Yn);
-  KST_LAUNCH(ctx);
-  KST_CUDA(ctx, cudaMemcpy2DAsync(Tb, sizeof(cplx) * ldV, Yn, sizeof(cplx) * s, sizeof(cplx) * s, n,
-                                  cudaMemcpyDeviceToDevice, st));
+  for (int pass = 0; pass < 2; ++pass) KST_TRY(step(Z, Z, Z, 1));
 
   bool converged = false;
   double prev_worst = 1e300;
   int stall = 0;
-  for (int it = 0; it < 80 && !converged; ++it) {
-    // W = Y - Z (Z^H Y), orthonormalised against Z
-    cplx* W = Vb + s;
-    KST_TRY(gram_ts(t, Vb, ldV, s, Tb, ldV, s, n, Cs));
-    KST_TRY(ts_mul(t, Vb, ldV, s, Cs, s, s, Tb, ldV, W, ldV, n));
-    KST_TRY(svqb(W, ldV, true, mask));
-    // BW
-    KST_CUDA(ctx, cudaMemcpy2DAsync(Wt, sizeof(cplx) * s, W, sizeof(cplx) * ldV, sizeof(cplx) * s,
-                                    n, cudaMemcpyDeviceToDevice, st));
-    bz_kernel<<<cdiv(n, BZ_ROWS), 128, 0, st>>>(M, n, Wt, s, Wt2);
-    KST_LAUNCH(ctx);
-    KST_CUDA(ctx, cudaMemcpy2DAsync(Tb + s, sizeof(cplx) * ldV, Wt2, sizeof(cplx) * s,
-                                    sizeof(cplx) * s, n, cudaMemcpyDeviceToDevice, st));
-    // Hred = V^H T, masked; eig
-    KST_TRY(gram_ts(t, Vb, ldV, s2, Tb, ldV, s2, n, H));
-    mask_hred_kernel<<<1, 256, 0, st>>>(H, s, mask, -1e300);
-    KST_LAUNCH(ctx);
-    KST_TRY(jacobi(ctx, H, s2, s2, 1.0, Hval, Hv, s2, st));
-    // Z = V C[:, :s], Y = T C[:, :s]
-    KST_TRY(ts_mul(t, Vb, ldV, s2, Hv, s2, s, nullptr, 0, Zn, s, n));
-    KST_TRY(ts_mul(t, Tb, ldV, s2, Hv, s2, s, nullptr, 0, Yn, s, n));
-    KST_CUDA(ctx, cudaMemcpy2DAsync(Vb, sizeof(cplx) * ldV, Zn, sizeof(cplx) * s, sizeof(cplx) * s,
-                                    n, cudaMemcpyDeviceToDevice, st));
-    KST_CUDA(ctx, cudaMemcpy2DAsync(Tb, sizeof(cplx) * ldV, Yn, sizeof(cplx) * s, sizeof(cplx) * s,
-                                    n, cudaMemcpyDeviceToDevice, st));
-    KST_CUDA(ctx, cudaMemcpyAsync(theta, Hval, sizeof(double) * s, cudaMemcpyDeviceToDevice, st));
-    ritz_residual_kernel<<<r, 256, 0, st>>>(Yn, Zn, n, s, theta, r, res);
-    KST_LAUNCH(ctx);
-    KST_CUDA(ctx, cudaMemcpyAsync(hres, res, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
-    KST_CUDA(ctx, cudaMemcpyAsync(hres + r, theta, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+  for (int it = 0; it < 60 && !converged; ++it) {
+    // two power steps per Rayleigh-Ritz (halves the sequential small steps)
+    KST_TRY(bz(ctx, M, n, Z, s, Y, st));
+    KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
+    cplx* Zcur = Z;
+    KST_TRY(step(Zcur, Y, Y2, 0));  // X = Ritz vectors of span(Zcur); Z <- orth(B^2 Zcur)
+    KST_TRY(step(Z, Z, Z, 1));      // second orthonormalisation pass
+    KST_CUDA(ctx, cudaMemcpyAsync(hres, res_part, sizeof(double) * nup * r, cudaMemcpyDeviceToHost, st));
+    KST_CUDA(ctx, cudaMemcpyAsync(hres + (size_t)nup * r, theta, sizeof(double) * s,
+                                  cudaMemcpyDeviceToHost, st));
+    KST_CUDA(ctx, cudaMemcpyAsync((int*)(hres + (size_t)nup * r + s), info, sizeof(int),
+                                  cudaMemcpyDeviceToHost, st));
     KST_CUDA(ctx, cudaStreamSynchronize(st));
+    const double* th = hres + (size_t)nup * r;
+    const int kept = *(int*)(hres + (size_t)nup * r + s);
     double tmax = 0.0, worst = 0.0;
-    for (int k = 0; k < s; ++k) tmax = std::max(tmax, std::fabs(hres[r + k]));
-    for (int k = 0; k < r; ++k) worst = std::max(worst, hres[k]);
-    if (tmax == 0.0 || worst <= 1e-12 * tmax) converged = true;
-    else if (worst <= 1e-9 * tmax) {
-      // accept a stalled residual floor once it stops improving
+    for (int k = 0; k < s; ++k) tmax = std::max(tmax, std::fabs(th[k]));
+    // Converged when every wanted Ritz pair has residual <= 1e-12 max|theta|
+    // (the FP64 floor), or <= 1e-9 max|theta| AND <= 1e-8 of its gap to the
+    // other Ritz values: eigenvector error <= residual / gap <= 1e-8.
+    bool all_ok = true;
+    for (int k = 0; k < r; ++k) {
+      double acc = 0.0;
+      for (int b = 0; b < nup; ++b) acc += hres[(size_t)b * r + k];
+      const double res = std::sqrt(acc);
+      worst = std::max(worst, res);
+      double gap = 1e300;
+      for (int jx = 0; jx < s; ++jx)
+        if (jx != k) gap = std::min(gap, std::fabs(th[k] - th[jx]));
+      all_ok = all_ok && (res <= 1e-12 * tmax || (res <= 1e-9 * tmax && res <= 1e-8 * gap));
+    }
+    if (kept == 0) break;  // B^2 Z vanished: leave it to the dense solver
+    if (tmax == 0.0 || all_ok) {
+      converged = true;
+    } else if (worst <= 1e-9 * tmax) {
+      // accept a residual floor once it stops improving
       stall = (worst > 0.5 * prev_worst) ? stall + 1 : 0;
       if (stall >= 3) converged = true;
     }
     prev_worst = worst;
   }
   if (!converged) return heig_top_cusolver(ctx, M, n, r, values_host, vectors, st);
-  finalize_top_kernel<<<1, 256, 0, st>>>(Zn, n, s, r, theta, vout, vectors);
+  finalize_top_kernel<<<1, 256, 0, st>>>(X, n, s, r, theta, vout, vectors);
   KST_LAUNCH(ctx);
   if (values_host) {
     KST_CUDA(ctx, cudaMemcpyAsync(values_host, vout, sizeof(double) * r, cudaMemcpyDeviceToHost, st));

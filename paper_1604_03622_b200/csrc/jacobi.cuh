@@ -100,7 +100,10 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
   }
   __syncthreads();
   const double fro = j.scratch[0];
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  // exact reciprocal-multiply division for the task maps (indices < 2^13, divisors <= 2^12)
+  const unsigned magic_n = 0xFFFFFFFFu / (unsigned)n + 1u;
+  const unsigned magic_pn = 0xFFFFFFFFu / (unsigned)(npairs * n) + 1u;
+  for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) *j.flag = 0;
     __syncthreads();
     for (int round = 0; round < m - 1; ++round) {
@@ -123,14 +126,20 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
         if (b < n) {
           const double app = j.A[a * j.ld + a].x, aqq = j.A[b * j.ld + b].x;
           const cplx apq = j.A[a * j.ld + b];
-          const double r = hypot(apq.x, apq.y);
-          const double thr = fmax(1e-17 * sqrt(fabs(app) * fabs(aqq)), 1e-300 + 1e-18 * fro);
-          if (r > thr) {
-            ec = apq.x / r;
-            es = apq.y / r;  // e^{i phi}
-            const double tau = (aqq - app) / (2.0 * r);
-            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = 1.0 / sqrt(1.0 + t * t);
+          const double r2 = apq.x * apq.x + apq.y * apq.y;
+          // skip rotations already at the rounding floor (relative to the pair
+          // and to |A|_F); a tighter floor only cycles on rounding noise.
+          // Compared squared: r > max(2.2e-16 sqrt|app aqq|, 1e-15 |A|_F).
+          const double thr2 = fmax(4.84e-32 * fabs(app) * fabs(aqq), 1e-600 + 1e-30 * fro * fro);
+          if (r2 > thr2) {
+            // rsqrt-based parameters: one division on the critical path
+            const double rinv = rsqrt(r2);
+            const double r = r2 * rinv;
+            ec = apq.x * rinv;
+            es = apq.y * rinv;  // e^{i phi}
+            const double tau = (aqq - app) * (0.5 * rinv);
+            const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
             // post-rotation diagonal (exact 2x2 values)
             j.scratch[2 * tid] = app - t * r;
@@ -148,9 +157,10 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
       __syncthreads();
       // column update: A <- A U, V <- V U on columns (p, q)
       for (int e = tid; e < npairs * n * 2; e += nt) {
-        const int mat = e / (npairs * n);
+        const int mat = (int)__umulhi((unsigned)e, magic_pn);  // e / (npairs * n)
         const int rem = e - mat * npairs * n;
-        const int k = rem / n, row = rem % n;
+        const int k = (int)__umulhi((unsigned)rem, magic_n);   // rem / n
+        const int row = rem - k * n;
         const int p = j.pp[k], q = j.pq[k];
         if (q >= n || j.s[k] == 0.0) continue;
         cplx* M = mat ? j.V : j.A;
@@ -164,7 +174,7 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
       __syncthreads();
       // row update: A <- U^H A on rows (p, q)
       for (int e = tid; e < npairs * n; e += nt) {
-        const int k = e / n, col = e % n;
+        const int k = (int)__umulhi((unsigned)e, magic_n), col = e - k * n;
         const int p = j.pp[k], q = j.pq[k];
         if (q >= n || j.s[k] == 0.0) continue;
         const double c = j.c[k], s = j.s[k];
@@ -188,6 +198,7 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
     }
     const int any = *j.flag;
     __syncthreads();
+    if (tid == 0) j.flag[1] = sweep + 1;  // diagnostic: sweeps used
     if (!any) break;
   }
   for (int i = tid; i < n; i += nt) j.val[i] = j.A[i * j.ld + i].x;

@@ -25,9 +25,21 @@ constexpr int NT = 256;
 constexpr int kMaxP = 16;
 constexpr int ST_ROWS = 8;   // rows of S per stats CTA
 constexpr int V_ROWS = 8;    // rows of S per V-step CTA
+constexpr int STAT_STRIDE = 4 + 2 * kMaxP;
+
+// Deterministic warp-strided sum of vals[k * stride], k < count: lane-fixed
+// partial sums then a fixed shuffle tree. Result valid in every lane.
+__device__ __forceinline__ double warp_sum_strided(const double* __restrict__ vals, int count,
+                                                   int stride) {
+  const int l = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int k = l; k < count; k += 32) acc += vals[(size_t)k * stride];
+  return warp_sum(acc);
+}
 
 // partial layout per CTA: [fro2, nonfinite, dmin, dmax, blocksum(j).re/im ...]
-__global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, int P, int q,
+template <int P>
+__global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, int q,
                                                    double* __restrict__ part) {
   __shared__ double sh[32];
   const int64_t d = (int64_t)P * q;
@@ -35,26 +47,22 @@ __global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, i
   const int r0 = blockIdx.x * ST_ROWS;         // row within block
   const int rows = min(ST_ROWS, q - r0);
   double fro = 0.0, bad = 0.0, dmin = 1e308, dmax = -1e308;
-  double bs[2 * kMaxP];
+  double bs[2 * P];
 #pragma unroll
-  for (int j = 0; j < 2 * kMaxP; ++j) bs[j] = 0.0;
+  for (int j = 0; j < 2 * P; ++j) bs[j] = 0.0;
   for (int rr = 0; rr < rows; ++rr) {
     const int64_t a = (int64_t)i * q + r0 + rr;
     const cplx* row = S + a * d;
 #pragma unroll
-    for (int j = 0; j < kMaxP; ++j) {
-      if (j >= P) break;
-      double sr = 0.0, si = 0.0;
+    for (int j = 0; j < P; ++j) {
       for (int c = threadIdx.x; c < q; c += NT) {
         const cplx v = row[(int64_t)j * q + c];
         if (!isfinite(v.x) || !isfinite(v.y)) bad += 1.0;
         fro = fma(v.x, v.x, fro);
         fro = fma(v.y, v.y, fro);
-        sr += v.x;
-        si += v.y;
+        bs[2 * j] += v.x;
+        bs[2 * j + 1] += v.y;
       }
-      bs[2 * j] += sr;
-      bs[2 * j + 1] += si;
     }
     if (threadIdx.x == 0) {
       const double dv = row[a].x;
@@ -62,7 +70,7 @@ __global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, i
       dmax = fmax(dmax, dv);
     }
   }
-  double* out = part + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * (4 + 2 * kMaxP);
+  double* out = part + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * STAT_STRIDE;
   fro = block_sum<NT>(fro, sh);
   bad = block_sum<NT>(bad, sh);
   if (threadIdx.x == 0) {
@@ -71,6 +79,7 @@ __global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, i
     out[2] = dmin;
     out[3] = dmax;
   }
+#pragma unroll
   for (int j = 0; j < 2 * P; ++j) {
     const double v = block_sum<NT>(bs[j], sh);
     if (threadIdx.x == 0) out[4 + j] = v;
@@ -84,58 +93,76 @@ struct IterState {
   int converged;
   int iteration;
   int pad;
-  cplx A[kMaxP * kMaxP];   // current spatial iterate (row-major P x P)
-  cplx Ainv[kMaxP * kMaxP];  // conj(A) / |A|^2 (b-step operand)
+  cplx A[kMaxP * kMaxP];     // current spatial iterate (row-major P x P)
+  cplx Aconj[kMaxP * kMaxP]; // conj(A) (b-step operand)
 };
 
-// Reduce stats partials -> fro, A0 (= blocksum / q^2), |A0|^2; diag checks.
-__global__ void init_kernel(const double* __restrict__ part, int nblk_x, int P, int q,
-                            IterState* st, double* host_diag) {
-  // single thread: fixed order
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double fro2 = 0.0, bad = 0.0, dmin = 1e308, dmax = -1e308;
-  for (int i = 0; i < P; ++i) {
-    double bsr[kMaxP], bsi[kMaxP];
-    for (int j = 0; j < P; ++j) bsr[j] = bsi[j] = 0.0;
-    for (int x = 0; x < nblk_x; ++x) {
-      const double* o = part + (size_t)(i * nblk_x + x) * (4 + 2 * kMaxP);
-      fro2 += o[0];
-      bad += o[1];
-      dmin = fmin(dmin, o[2]);
-      dmax = fmax(dmax, o[3]);
-      for (int j = 0; j < P; ++j) {
-        bsr[j] += o[4 + 2 * j];
-        bsi[j] += o[4 + 2 * j + 1];
-      }
+// Reduce stats partials -> fro, A0 (= blocksum / q^2), |A0|^2; diag stats.
+// One CTA; every sum is a fixed-order warp reduction (deterministic).
+__global__ void __launch_bounds__(NT) init_kernel(const double* __restrict__ part, int nblk_x,
+                                                  int P, int q, IterState* st, double* host_diag) {
+  __shared__ double red[4 + 2 * kMaxP * kMaxP];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nrec = nblk_x * P;
+  const int nq = 2 + 2 * P * P;  // fro2, bad, then A0 re/im per (i, j)
+  for (int k = w; k < nq; k += NT / 32) {
+    double v;
+    if (k < 2) {
+      v = warp_sum_strided(part + k, nrec, STAT_STRIDE);
+    } else {
+      const int e = (k - 2) >> 1, ri = (k - 2) & 1;
+      const int i = e / P, j = e % P;
+      v = warp_sum_strided(part + (size_t)i * nblk_x * STAT_STRIDE + 4 + 2 * j + ri, nblk_x,
+                           STAT_STRIDE);
     }
-    for (int j = 0; j < P; ++j)
-      st->A[i * P + j] = cmk(bsr[j] / (double)(q * (double)q), bsi[j] / (double)(q * (double)q));
+    if (l == 0) red[k] = v;
   }
-  double na2 = 0.0;
-  for (int e = 0; e < P * P; ++e) na2 += cabs2(st->A[e]);
-  st->fro2 = fro2;
-  st->fro = sqrt(fro2);
-  st->na2 = na2;
-  st->eta_prev = INFINITY;
-  st->status = 0;
-  st->converged = 0;
-  st->iteration = 0;
-  for (int e = 0; e < P * P; ++e)
-    st->Ainv[e] = cmk(st->A[e].x, -st->A[e].y);
-  host_diag[0] = bad;
-  host_diag[1] = dmin;
-  host_diag[2] = dmax;
-  host_diag[3] = st->fro;
-  host_diag[4] = na2;
+  if (w == 0) {
+    double mn = 1e308, mx = -1e308;
+    for (int k = l; k < nrec; k += 32) {
+      mn = fmin(mn, part[(size_t)k * STAT_STRIDE + 2]);
+      mx = fmax(mx, part[(size_t)k * STAT_STRIDE + 3]);
+    }
+    mn = warp_min(mn);
+    mx = warp_max(mx);
+    if (l == 0) {
+      red[nq] = mn;
+      red[nq + 1] = mx;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double qq = (double)q * (double)q;
+    double na2 = 0.0;
+    for (int e = 0; e < P * P; ++e) {
+      const cplx a = cmk(red[2 + 2 * e] / qq, red[3 + 2 * e] / qq);
+      st->A[e] = a;
+      st->Aconj[e] = cmk(a.x, -a.y);
+      na2 += cabs2(a);
+    }
+    st->fro2 = red[0];
+    st->fro = sqrt(red[0]);
+    st->na2 = na2;
+    st->eta_prev = INFINITY;
+    st->status = 0;
+    st->converged = 0;
+    st->iteration = 0;
+    host_diag[0] = red[1];
+    host_diag[1] = red[nq];
+    host_diag[2] = red[nq + 1];
+    host_diag[3] = st->fro;
+    host_diag[4] = na2;
+  }
 }
 
 // b[r,c] = sum_ij S4[i,r,j,c] conj(A[i,j]) / |A|^2 ; partial |b|^2 per CTA
-__global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, int P, int q,
+template <int P>
+__global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, int q,
                                                    const IterState* __restrict__ st,
                                                    cplx* __restrict__ b, double* __restrict__ part) {
-  __shared__ cplx ca[kMaxP * kMaxP];
+  __shared__ cplx ca[P * P];
   __shared__ double sh[32];
-  for (int e = threadIdx.x; e < P * P; e += NT) ca[e] = st->Ainv[e];
+  for (int e = threadIdx.x; e < P * P; e += NT) ca[e] = st->Aconj[e];
   __syncthreads();
   const double na2 = st->na2;
   const int64_t d = (int64_t)P * q;
@@ -144,8 +171,10 @@ __global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, i
   double nb = 0.0;
   if (c < q) {
     cplx acc = cmk(0, 0);
+#pragma unroll
     for (int i = 0; i < P; ++i) {
       const cplx* row = S + ((int64_t)i * q + r) * d + c;
+#pragma unroll
       for (int j = 0; j < P; ++j) cfma(acc, row[(int64_t)j * q], ca[i * P + j]);
     }
     acc = cmk(acc.x / na2, acc.y / na2);
@@ -157,7 +186,8 @@ __global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, i
 }
 
 // V partials: CTA (x = row chunk, y = block row i) -> part[(i, x)][j]
-__global__ void __launch_bounds__(NT) vstep_kernel(const cplx* __restrict__ S, int P, int q,
+template <int P>
+__global__ void __launch_bounds__(NT) vstep_kernel(const cplx* __restrict__ S, int q,
                                                    const cplx* __restrict__ b,
                                                    cplx* __restrict__ part) {
   __shared__ double sh[32];
@@ -165,9 +195,9 @@ __global__ void __launch_bounds__(NT) vstep_kernel(const cplx* __restrict__ S, i
   const int i = blockIdx.y;
   const int r0 = blockIdx.x * V_ROWS;
   const int rows = min(V_ROWS, q - r0);
-  double ar[kMaxP], ai[kMaxP];
+  double ar[P], ai[P];
 #pragma unroll
-  for (int j = 0; j < kMaxP; ++j) ar[j] = ai[j] = 0.0;
+  for (int j = 0; j < P; ++j) ar[j] = ai[j] = 0.0;
   for (int rr = 0; rr < rows; ++rr) {
     const int r = r0 + rr;
     const cplx* row = S + ((int64_t)i * q + r) * d;
@@ -175,19 +205,18 @@ __global__ void __launch_bounds__(NT) vstep_kernel(const cplx* __restrict__ S, i
     for (int c = threadIdx.x; c < q; c += NT) {
       const cplx bv = brow[c];
 #pragma unroll
-      for (int j = 0; j < kMaxP; ++j) {
-        if (j < P) {
-          const cplx s = row[(int64_t)j * q + c];
-          // s * conj(bv)
-          ar[j] = fma(s.x, bv.x, ar[j]);
-          ar[j] = fma(s.y, bv.y, ar[j]);
-          ai[j] = fma(s.y, bv.x, ai[j]);
-          ai[j] = fma(-s.x, bv.y, ai[j]);
-        }
+      for (int j = 0; j < P; ++j) {
+        const cplx s = row[(int64_t)j * q + c];
+        // s * conj(bv)
+        ar[j] = fma(s.x, bv.x, ar[j]);
+        ar[j] = fma(s.y, bv.y, ar[j]);
+        ai[j] = fma(s.y, bv.x, ai[j]);
+        ai[j] = fma(-s.x, bv.y, ai[j]);
       }
     }
   }
   cplx* out = part + (size_t)(blockIdx.y * gridDim.x + blockIdx.x) * P;
+#pragma unroll
   for (int j = 0; j < P; ++j) {
     const double re = block_sum<NT>(ar[j], sh);
     const double im = block_sum<NT>(ai[j], sh);
@@ -207,17 +236,26 @@ __global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart
   __shared__ double lam[kMaxP];
   __shared__ double nb2_s;
   __shared__ int bad_s;
+  __shared__ double red_sh[32];
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    double nb2 = 0.0;
-    for (int k = 0; k < nbp; ++k) nb2 += bpart[k];
-    nb2_s = nb2;
+  {
+    double acc = 0.0;
+    for (int k = tid; k < nbp; k += NT) acc += bpart[k];
+    acc = block_sum<NT>(acc, red_sh);
+    if (tid == 0) nb2_s = acc;
   }
-  for (int e = tid; e < P * P; e += NT) {
-    const int i = e / P, j = e % P;
-    cplx acc = cmk(0, 0);
-    for (int x = 0; x < nvx; ++x) acc = cadd(acc, vpart[(size_t)(i * nvx + x) * P + j]);
-    V[e] = acc;
+  {
+    const int w = tid >> 5, l = tid & 31;
+    for (int k = w; k < 2 * P * P; k += NT / 32) {
+      const int e = k >> 1, ri = k & 1;
+      const int i = e / P, j = e % P;
+      const double v = warp_sum_strided((const double*)vpart + ((size_t)i * nvx * P + j) * 2 + ri,
+                                        nvx, 2 * P);
+      if (l == 0) {
+        if (ri) V[e].y = v;
+        else V[e].x = v;
+      }
+    }
   }
   __syncthreads();
   const double nb2 = nb2_s;
@@ -301,7 +339,7 @@ __global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart
     for (int e = 0; e < P * P; ++e) {
       st->A[e] = Anew[e];
       spatial_out[e] = Anew[e];
-      st->Ainv[e] = cmk(Anew[e].x, -Anew[e].y);
+      st->Aconj[e] = cmk(Anew[e].x, -Anew[e].y);
     }
     host_out[0] = 0;
     host_out[1] = eta;
@@ -328,7 +366,7 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   const int64_t d = (int64_t)p * q;
   // stats pass
   const int nbx = (q + ST_ROWS - 1) / ST_ROWS;
-  const size_t stat_stride = 4 + 2 * kMaxP;
+  const size_t stat_stride = STAT_STRIDE;
   const int nvx = (q + V_ROWS - 1) / V_ROWS;
   const int nbb = (q + NT - 1) / NT;
   char* small = (char*)ws_get(ctx, WS_SMALL, sizeof(IterState) + 256);
@@ -341,9 +379,9 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   if (!small || !part || !b || !hbuf) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");
   IterState* state = (IterState*)small;
 
-  stats_kernel<<<dim3(nbx, p), NT, 0, st>>>(S, p, q, part);
+  KST_DISPATCH_P(p, (stats_kernel<PP><<<dim3(nbx, p), NT, 0, st>>>(S, q, part)));
   KST_LAUNCH(ctx);
-  init_kernel<<<1, 32, 0, st>>>(part, nbx, p, q, state, (double*)(small + sizeof(IterState)));
+  init_kernel<<<1, NT, 0, st>>>(part, nbx, p, q, state, (double*)(small + sizeof(IterState)));
   KST_LAUNCH(ctx);
   KST_CUDA(ctx, cudaMemcpyAsync(hbuf, small + sizeof(IterState), 5 * sizeof(double),
                                 cudaMemcpyDeviceToHost, st));
@@ -388,9 +426,9 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   for (int it = 0; it < max_iter; ++it) {
     if (na2 == 0.0) return set_err(ctx, KST_ERR_DEGENERATE, "spatial iterate collapsed to zero");
     ++iters;
-    bstep_kernel<<<dim3(nbb, q), NT, 0, st>>>(S, p, q, state, b, bpart);
+    KST_DISPATCH_P(p, (bstep_kernel<PP><<<dim3(nbb, q), NT, 0, st>>>(S, q, state, b, bpart)));
     KST_LAUNCH(ctx);
-    vstep_kernel<<<dim3(nvx, p), NT, 0, st>>>(S, p, q, b, vpart);
+    KST_DISPATCH_P(p, (vstep_kernel<PP><<<dim3(nvx, p), NT, 0, st>>>(S, q, b, vpart)));
     KST_LAUNCH(ctx);
     tail_kernel<<<1, NT, tail_smem, st>>>(vpart, nvx, bpart, nbb * q, p, ra, tol, state, spatial, hout);
     KST_LAUNCH(ctx);

@@ -158,7 +158,8 @@ def test_multipass_matches_reference():
         st = kst.stack_passes(hist)
         est = kst.multipass_estimate(st, int(g[f"{name}__rb"]))
         assert est.iterations == int(g[f"{name}__iterations"])
-        np.testing.assert_allclose(est.residuals, g[f"{name}__residuals"], rtol=1e-9)
+        # identical noiseless passes fit exactly: residuals sit on the sqrt(eps) floor
+        np.testing.assert_allclose(est.residuals, g[f"{name}__residuals"], rtol=1e-9, atol=1e-7)
         filt = kst.build_filter("kron", estimate=est)
         imgs = kst.pass_images(filt, st, kst.make_doppler_grid(int(g[f"{name}__D"])),
                                spatial_count=int(g[f"{name}__G"]))

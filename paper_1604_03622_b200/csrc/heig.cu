@@ -52,18 +52,40 @@ __global__ void __launch_bounds__(128) bz_kernel(const cplx* __restrict__ B, int
   const int t = threadIdx.x;
   const int row = t >> 3, cg = t & 7;  // 16 rows x 8 column groups
   cplx acc[4] = {cmk(0, 0), cmk(0, 0), cmk(0, 0), cmk(0, 0)};
-  for (int k0 = kbeg; k0 < kend; k0 += BZ_K) {
-    for (int e = t; e < BZ_ROWS * BZ_K; e += 128) {
+  // register prefetch of the next chunk (global loads overlap the compute)
+  cplx pb[4], pz[8];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = t + 128 * u;
       const int rr = e / BZ_K, kk = e % BZ_K;
       const int gr = r0 + rr, gk = k0 + kk;
-      sb[rr][kk] = (gr < n && gk < kend) ? B[(size_t)gr * n + gk] : cmk(0, 0);
+      pb[u] = (gr < n && gk < kend) ? B[(size_t)gr * n + gk] : cmk(0, 0);
     }
-    for (int e = t; e < BZ_K * s; e += 128) {
-      const int kk = e / s, c = e % s;
-      const int gk = k0 + kk;
-      sz[kk][c] = gk < kend ? Z[(size_t)gk * s + c] : cmk(0, 0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = t + 128 * u;
+      if (e < BZ_K * s) {
+        const int kk = e / s, c = e % s;
+        const int gk = k0 + kk;
+        pz[u] = gk < kend ? Z[(size_t)gk * s + c] : cmk(0, 0);
+      }
+    }
+  };
+  fetch(kbeg);
+  for (int k0 = kbeg; k0 < kend; k0 += BZ_K) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = t + 128 * u;
+      sb[e / BZ_K][e % BZ_K] = pb[u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = t + 128 * u;
+      if (e < BZ_K * s) sz[e / s][e % s] = pz[u];
     }
     __syncthreads();
+    if (k0 + BZ_K < kend) fetch(k0 + BZ_K);
     // only the column groups this thread owns (no predicated-off DFMAs)
     const int ncol = (s - cg + 7) >> 3;
 #define BZ_CASE(NC)                                                      \
@@ -89,6 +111,55 @@ __global__ void __launch_bounds__(128) bz_kernel(const cplx* __restrict__ B, int
       const int col = cg + 8 * c;
       if (col < s) Y[(size_t)gr * s + col] = acc[c];
     }
+  }
+}
+
+// Y = B Z for Hermitian B via Y[i, c] = conj(sum_k conj(Z[k, c]) B[k, i]):
+// thread i streams column i of B down rows k (coalesced across the warp, each
+// element read once, 8 loads in flight per thread), Z rows broadcast from
+// shared memory. Split-K over blockIdx.y; partials summed in fixed order.
+constexpr int BZ2_COLS = 128;
+template <int S>
+struct Bz2K {
+  static constexpr int value = S <= 16 ? 128 : 64;  // keeps sz under 48 KB
+};
+template <int S>
+__global__ void __launch_bounds__(BZ2_COLS) bz2_kernel(const cplx* __restrict__ B, int n,
+                                                        const cplx* __restrict__ Z,
+                                                        cplx* __restrict__ Ypart) {
+  constexpr int BZ2_K = Bz2K<S>::value;
+  __shared__ cplx sz[BZ2_K * S];
+  const int i = blockIdx.x * BZ2_COLS + threadIdx.x;
+  const int kbeg = blockIdx.y * BZ2_K, kend = min(n, kbeg + BZ2_K);
+  for (int e = threadIdx.x; e < (kend - kbeg) * S; e += BZ2_COLS)
+    sz[e] = cconj(Z[(size_t)kbeg * S + e]);
+  __syncthreads();
+  cplx acc[S];
+#pragma unroll
+  for (int c = 0; c < S; ++c) acc[c] = cmk(0, 0);
+  if (i < n) {
+    const cplx* col = B + i;
+    int k = kbeg;
+    for (; k + 8 <= kend; k += 8) {
+      cplx bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) bv[u] = col[(size_t)(k + u) * n];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const cplx* zr = sz + (k + u - kbeg) * S;
+#pragma unroll
+        for (int c = 0; c < S; ++c) cfma(acc[c], zr[c], bv[u]);
+      }
+    }
+    for (; k < kend; ++k) {
+      const cplx bv = col[(size_t)k * n];
+      const cplx* zr = sz + (k - kbeg) * S;
+#pragma unroll
+      for (int c = 0; c < S; ++c) cfma(acc[c], zr[c], bv);
+    }
+    cplx* Y = Ypart + (size_t)blockIdx.y * n * S + (size_t)i * S;
+#pragma unroll
+    for (int c = 0; c < S; ++c) Y[c] = cconj(acc[c]);
   }
 }
 
@@ -204,6 +275,55 @@ __global__ void random_block_kernel(cplx* Z, int n, int s, uint64_t seed) {
     const double u2 = ((y >> 11) + 0.5) * (1.0 / 9007199254740992.0);
     Z[e] = cmk(u1 - 0.5, u2 - 0.5);
   }
+}
+
+// Z0 (n x s) = unit vectors e_i for the s largest Re(B_ii) (ties -> lower i).
+__global__ void unit_start_kernel(const cplx* __restrict__ B, int n, int s, cplx* __restrict__ Z) {
+  __shared__ int picked[32];
+  __shared__ double bv[8];
+  __shared__ int bi[8];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < n * s; e += blockDim.x) Z[e] = cmk(0, 0);
+  for (int k = 0; k < s; ++k) {
+    double best = -INFINITY;
+    int besti = n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      bool used = false;
+      for (int j = 0; j < k; ++j) used |= picked[j] == i;
+      const double v = B[(size_t)i * n + i].x;
+      if (!used && (v > best || (v == best && i < besti))) {
+        best = v;
+        besti = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+      if (ob > best || (ob == best && oi < besti)) {
+        best = ob;
+        besti = oi;
+      }
+    }
+    if (l == 0) {
+      bv[w] = best;
+      bi[w] = besti;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b0 = bv[0];
+      int i0 = bi[0];
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+        if (bv[q] > b0 || (bv[q] == b0 && bi[q] < i0)) {
+          b0 = bv[q];
+          i0 = bi[q];
+        }
+      if (i0 >= n) i0 = k;  // fewer candidates than s (cannot happen for n > 64)
+      picked[k] = i0;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (threadIdx.x < s) Z[(size_t)picked[threadIdx.x] * s + threadIdx.x] = cmk(1.0, 0.0);
 }
 
 // Final ordering (descending, reference tie rule) + pivot phase for the top r
@@ -634,6 +754,23 @@ int ts_mul(TsCtx& t, const cplx* U, int ldu, int s1, const cplx* C, int ldc, int
 }
 
 int bz(kst_ctx* ctx, const cplx* B, int n, const cplx* Z, int s, cplx* Y, cudaStream_t st) {
+  if (s % 8 == 0 && s <= 32) {
+    const int kc = s <= 16 ? 128 : 64;
+    const int ks = (n + kc - 1) / kc;
+    cplx* part = (cplx*)ws_get(ctx, WS_BZ, sizeof(cplx) * (size_t)ks * n * s);
+    if (!part) return set_err(ctx, KST_ERR_CUDA, "bz: workspace");
+    const dim3 grid(cdiv(n, BZ2_COLS), ks);
+    switch (s) {
+      case 8: bz2_kernel<8><<<grid, BZ2_COLS, 0, st>>>(B, n, Z, part); break;
+      case 16: bz2_kernel<16><<<grid, BZ2_COLS, 0, st>>>(B, n, Z, part); break;
+      case 24: bz2_kernel<24><<<grid, BZ2_COLS, 0, st>>>(B, n, Z, part); break;
+      default: bz2_kernel<32><<<grid, BZ2_COLS, 0, st>>>(B, n, Z, part); break;
+    }
+    KST_LAUNCH(ctx);
+    reduce_partials_kernel<<<grid_for((int64_t)n * s), 256, 0, st>>>(part, ks, n * s, Y);
+    KST_LAUNCH(ctx);
+    return KST_OK;
+  }
   const int ks = (n + BZ_KSPLIT - 1) / BZ_KSPLIT;
   cplx* part = (cplx*)ws_get(ctx, WS_BZ, sizeof(cplx) * (size_t)ks * n * s);
   if (!part) return set_err(ctx, KST_ERR_CUDA, "bz: workspace");
@@ -787,7 +924,7 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   if (r > 24) return heig_top_cusolver(ctx, M, n, r, values_host, vectors, st);
 
   // block: r wanted + >= 5 guard vectors (convergence rate lambda_{s+1}/lambda_r)
-  const int s = std::min(32, std::max(8, r + 5));
+  const int s = std::min(32, ((std::max(8, r + 5) + 7) / 8) * 8);
   const size_t nb = (size_t)n * s;
   const int nblk = std::min((n + K4_ROWS - 1) / K4_ROWS, 32);
   const int nup = (n + 7) / 8;
@@ -830,10 +967,10 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     std::swap(Z, Zn);  // Zn (= Y2 C) becomes the current block
     return KST_OK;
   };
-  // Z0 = orth(random), two orthonormalisation passes
-  random_block_kernel<<<grid_for((int64_t)n * s), 256, 0, st>>>(Z, n, s, 0x5EEDull + n);
+  // Z0 = unit vectors at the s largest diagonal entries of B (orthonormal by
+  // construction; B e_i is the i-th column, rich in the dominant directions)
+  unit_start_kernel<<<1, 256, 0, st>>>(M, n, s, Z);
   KST_LAUNCH(ctx);
-  for (int pass = 0; pass < 2; ++pass) KST_TRY(step(Z, Z, Z, 1));
 
   bool converged = false;
   double prev_worst = 1e300;
@@ -844,15 +981,15 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
     cplx* Zcur = Z;
     KST_TRY(step(Zcur, Y, Y2, 0));  // X = Ritz vectors of span(Zcur); Z <- orth(B^2 Zcur)
-    KST_TRY(step(Z, Z, Z, 1));      // second orthonormalisation pass
     KST_CUDA(ctx, cudaMemcpyAsync(hres, res_part, sizeof(double) * nup * r, cudaMemcpyDeviceToHost, st));
     KST_CUDA(ctx, cudaMemcpyAsync(hres + (size_t)nup * r, theta, sizeof(double) * s,
                                   cudaMemcpyDeviceToHost, st));
-    KST_CUDA(ctx, cudaMemcpyAsync((int*)(hres + (size_t)nup * r + s), info, sizeof(int),
+    KST_CUDA(ctx, cudaMemcpyAsync((int*)(hres + (size_t)nup * r + s), info, 2 * sizeof(int),
                                   cudaMemcpyDeviceToHost, st));
     KST_CUDA(ctx, cudaStreamSynchronize(st));
     const double* th = hres + (size_t)nup * r;
     const int kept = *(int*)(hres + (size_t)nup * r + s);
+    const int path = *((int*)(hres + (size_t)nup * r + s) + 1);
     double tmax = 0.0, worst = 0.0;
     for (int k = 0; k < s; ++k) tmax = std::max(tmax, std::fabs(th[k]));
     // Converged when every wanted Ritz pair has residual <= 1e-12 max|theta|
@@ -878,6 +1015,9 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
       if (stall >= 3) converged = true;
     }
     prev_worst = worst;
+    // the SVQB path (ill-conditioned block) regenerates noise directions that
+    // need a second orthonormalisation; the Cholesky path is already orthonormal
+    if (!converged && path != 2) KST_TRY(step(Z, Z, Z, 1));
   }
   if (!converged) return heig_top_cusolver(ctx, M, n, r, values_host, vectors, st);
   finalize_top_kernel<<<1, 256, 0, st>>>(X, n, s, r, theta, vout, vectors);

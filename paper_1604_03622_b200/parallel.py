@@ -1,0 +1,70 @@
+"""Multi-GPU frame sharding (SURVEY.md §8e, configs[2]).
+
+Frames of a sequence are independent units: rank r processes frames
+r, r + W, r + 2W, ... (round robin) with the single-GPU pipeline and no
+data-path collective. The only collective is the optional gather of the
+detection maps to rank 0 (NCCL over NVLink on the GPU box; gloo works the
+same way for the CPU tests). One process per GPU, launched by torchrun.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def frame_assignment(n_frames, world):
+    """Frame indices per rank, round robin (deterministic)."""
+    if n_frames < 0 or world < 1:
+        raise ValueError("n_frames >= 0 and world >= 1 required")
+    return [list(range(r, n_frames, world)) for r in range(world)]
+
+
+def local_frames(n_frames, rank, world):
+    return frame_assignment(n_frames, world)[rank]
+
+
+def gather_maps(local_maps, n_frames, group=None, dst_all=True):
+    """All-gather per-rank map stacks into the global frame order.
+
+    local_maps: tensor (k_local, n, D) holding this rank's frames in the order
+    of `local_frames`. Ranks with fewer frames are padded to the per-rank
+    maximum (all_gather needs equal shapes). Returns (n_frames, n, D) on
+    every rank (or None off rank 0 when dst_all is False).
+    """
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per = -(-n_frames // world) if n_frames else 0
+    k_local, *tail = local_maps.shape
+    assert k_local == len(local_frames(n_frames, rank, world))
+    pad = torch.zeros((per, *tail), dtype=local_maps.dtype, device=local_maps.device)
+    pad[:k_local] = local_maps
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    if not dst_all and rank != 0:
+        return None
+    out = torch.empty((n_frames, *tail), dtype=local_maps.dtype, device=local_maps.device)
+    for r, frames in enumerate(frame_assignment(n_frames, world)):
+        for j, f in enumerate(frames):
+            out[f] = bufs[r][j]
+    return out
+
+
+def process_sequence(frames, rank_spatial=1, rank_temporal=3, dopplers=None, spatial_grid=None,
+                     group=None, gather=True, **kw):
+    """Run the fused pipeline over this rank's share of `frames` (a list of
+    (n, p, q) cubes, numpy or CUDA) and optionally gather all maps."""
+    from .pipeline import process_frame
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    mine = local_frames(len(frames), rank, world)
+    maps = []
+    for f in mine:
+        vals, _ = process_frame(frames[f], rank_spatial, rank_temporal, dopplers, spatial_grid, **kw)
+        maps.append(torch.as_tensor(vals))
+    if not gather or world == 1:
+        return maps
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+        else torch.device("cpu")
+    local = torch.stack([m.to(dev) for m in maps]) if maps else torch.zeros((0,), device=dev)
+    return gather_maps(local, len(frames), group)

@@ -1,0 +1,69 @@
+"""CPU, world_size 2 over gloo: the frame-sharding host logic of the N > 1
+path (paper_1604_03622_b200/parallel.py). Each rank computes its frames'
+maps with the CPU oracle standing in for the GPU pipeline (test only), then
+the maps are gathered into global frame order and checked on every rank."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1604_03622_b200 import parallel
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _frames():
+    from paper_1604_03622_b200 import scenes
+    return [scenes.bench_scene(3, 16, 24, seed=100 + f, movers=1).data[0] for f in range(5)]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import kron_oracle as orc
+        frames = _frames()
+        mine = parallel.local_frames(len(frames), rank, world)
+        maps = [torch.from_numpy(orc.pipeline(frames[f], 1, 3, 16)[3]) for f in mine]
+        local = torch.stack(maps)
+        full = parallel.gather_maps(local, len(frames))
+        want = np.stack([orc.pipeline(fr, 1, 3, 16)[3] for fr in frames])
+        q.put((rank, bool(np.array_equal(full.numpy(), want)), mine))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_frame_assignment_is_a_partition():
+    for n, w in ((0, 1), (5, 2), (100, 8), (3, 4)):
+        parts = parallel.frame_assignment(n, w)
+        flat = sorted(f for p in parts for f in p)
+        assert flat == list(range(n))
+        assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gather_reassembles_frame_order():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r for r, _, _ in res) == [0, 1]
+    assert all(ok for _, ok, _ in res)
+    assert {r: m for r, _, m in res} == {0: [0, 2, 4], 1: [1, 3]}

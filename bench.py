@@ -126,14 +126,55 @@ def fp64_peak_tflops():
         return 37.2, "spec-derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
 
 
-def ncu_traffic():
-    path = os.path.join(ROOT, "profiles", "gram_ncu.json")
+def ncu_traffic(name):
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             d = json.load(f)
         return d.get("dram_bytes_per_launch"), d
     except (OSError, ValueError):
         return None, None
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def fp64_roofline(flops, gram_ms):
+    peak, peak_src = fp64_peak_tflops()
+    traffic, _ = ncu_traffic("gram_ncu.json")
+    achieved = flops / (gram_ms * 1e-3) / 1e12
+    return {"kernel": "gram_herm_dmma (K1, sample covariance, FP64 DMMA engine)", "bound": "fp64",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": traffic,
+            "algorithmic": f"4*n*(pq)^2 = {flops:.4e} flop per launch (8 flop per complex MAC, "
+                           "Hermitian half)",
+            "executed_tflops": 0.75 * achieved, "executed_frac": 0.75 * achieved / peak,
+            "executed_note": "3M complex product: 6 real flop per complex MAC are executed",
+            "peak_source": peak_src}
+
+
+def int8_roofline(ops, gemm_ms, slices, flops, gram_ms):
+    """Dominant kernel of the int8 engine: the slice GEMMs on the int8 tensor
+    cores (int8 ops per Gram / GEMM span). Peak: 2 x the measured dense bf16
+    rate in MEASURED_PEAKS.json (B200 int8 dense = 2 x bf16 dense)."""
+    pk = measured_peaks()
+    peak = 2.0 * pk.get("bf16_tflops_sustained", 1376.6)
+    traffic, _ = ncu_traffic("gram_int8_ncu.json")
+    achieved = ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    return {"kernel": f"int8 slice GEMMs of K1 (sample covariance, {slices} slices, tensor cores)",
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
+            "frac": achieved / peak, "traffic": traffic,
+            "algorithmic": f"2*dpad^2*npad*3*s(s+1)/2 = {ops:.4e} int8 ops per Gram "
+                           f"(exact slice products for the {flops:.4e}-flop complex Gram)",
+            "gemm_span_ms": gemm_ms, "gram_stage_ms": gram_ms,
+            "fp64_equivalent_tflops": flops / (gram_ms * 1e-3) / 1e12,
+            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 dense = 2 x bf16 "
+                           "dense on B200); cuBLAS int8 measured 3.03 POPS here (tools/int8_probe.py)"}
 
 
 def cpu_threads():
@@ -277,12 +318,14 @@ def main():
     e2e_value = px_step * args.steps / (e2e_tot / 1e3)
 
     if rank == 0:
-        st = np.mean(np.stack(stages), axis=0)
+        st = np.mean(np.stack([np.pad(x, (0, 8 - len(x))) for x in stages]), axis=0)
         gram_ms = float(st[0])
         flops = 4.0 * n * float(p * q) ** 2          # Hermitian half, 8 flop per complex MAC
-        peak, peak_src = fp64_peak_tflops()
-        traffic, _ = ncu_traffic()
-        achieved = flops / (gram_ms * 1e-3) / 1e12
+        engine, slices = kst.lrkron.get_gram_engine(dev)
+        if engine == "int8":
+            roof = int8_roofline(lib.kst_gram_int8_ops(c), float(st[5]), slices, flops, gram_ms)
+        else:
+            roof = fp64_roofline(flops, gram_ms)
         line = {
             "metric": "STAP pixels/sec", "value": value, "unit": "pixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps,
@@ -292,16 +335,8 @@ def main():
             "stages_ms": {"scm": gram_ms, "lrkron": float(st[1]), "bases": float(st[2]),
                           "detect": float(st[3])},
             "iterations": int(statistics.median(iters)),
-            "roofline": {"kernel": "gram_herm (K1, sample covariance)", "bound": "fp64",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic": f"4*n*(pq)^2 = {flops:.4e} flop per launch "
-                                        "(8 flop per complex MAC, Hermitian half)",
-                         "executed_tflops": 0.75 * achieved,
-                         "executed_frac": 0.75 * achieved / peak,
-                         "executed_note": "3M complex product: 6 real flop per complex MAC are "
-                                          "executed, so executed = 0.75 x algorithmic",
-                         "peak_source": peak_src},
+            "gram_engine": {"mode": engine, "slices": slices},
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "pixels/s",
                     "h2d_bytes_per_step": int(host_cubes[0].nbytes),
                     "d2h_bytes_per_step": int(n * D * 8)},

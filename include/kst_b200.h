@@ -58,6 +58,18 @@ int kst_version(void);
  *   boundaries; kst_stage_times then returns up to `max` stage durations in
  *   ms (scm, lrkron, bases, detect) of the last call, and the count. */
 long long kst_launch_count(const kst_ctx* ctx);
+
+/* Sample-covariance engine (K1). mode 0: FP64 tensor-core DMMA tiles (FP64
+ * rounding only). mode 1: int8 tensor-core GEMMs on exact 7-bit slices
+ * (`slices` per operand, 3..8; relative error ~(slices+1) 2^-7*slices of
+ * max|x_a| max|x_b| n). Default: mode 1 with 6 slices when cuBLAS is
+ * loadable (else mode 0); env KST_GRAM=dmma|int8 and KST_GRAM_SLICES
+ * override it at context creation. */
+int kst_set_gram(kst_ctx* ctx, int mode, int slices);
+int kst_get_gram(const kst_ctx* ctx, int* mode, int* slices);
+/* int8 tensor ops issued by the last int8 Gram (0 if none); with profiling on,
+ * kst_stage_times entry 5 is that Gram's int8 GEMM span in ms. */
+double kst_gram_int8_ops(const kst_ctx* ctx);
 int kst_set_profiling(kst_ctx* ctx, int on);
 int kst_stage_times(kst_ctx* ctx, double* ms, int max);
 

@@ -29,6 +29,9 @@ _SIGS = {
     "kst_ctx_destroy": (_i, [_vp]),
     "kst_last_error": (C.c_char_p, [_vp]),
     "kst_launch_count": (C.c_longlong, [_vp]),
+    "kst_set_gram": (_i, [_vp, _i, _i]),
+    "kst_get_gram": (_i, [_vp, _ip, _ip]),
+    "kst_gram_int8_ops": (_d, [_vp]),
     "kst_set_profiling": (_i, [_vp, _i]),
     "kst_stage_times": (_i, [_vp, _vp, _i]),
     "kst_scm": (_i, [_vp, _vp, _i64, _i64, _vp, _vp]),

@@ -1,6 +1,8 @@
 // C ABI of libkst_b200.so (declared in include/kst_b200.h): context,
 // workspace and the extern "C" entry points. No C++ exception crosses it.
+#include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -90,6 +92,13 @@ int kst_ctx_create(int device, kst_ctx** out) {
   kst_ctx* c = new (std::nothrow) kst_ctx();
   if (!c) return KST_ERR_CUDA;
   c->device = device;
+  // K1 engine default: int8 tensor-core slices (6 x 7 bits: S relative error
+  // ~1e-11, see gram_ozaki.cu) when cuBLAS is loadable, else FP64 DMMA.
+  // Override: KST_GRAM=int8|dmma, KST_GRAM_SLICES=3..8.
+  c->gram_slices = 6;
+  c->gram_mode = kst::ozaki_available() ? 1 : 0;
+  if (const char* e = getenv("KST_GRAM")) c->gram_mode = (strcmp(e, "int8") == 0 && kst::ozaki_available()) ? 1 : 0;
+  if (const char* e = getenv("KST_GRAM_SLICES")) c->gram_slices = std::min(8, std::max(3, atoi(e)));
   DeviceGuard g(device);
   cudaFree(nullptr);  // establish the primary context
   *out = c;
@@ -114,6 +123,27 @@ int kst_ctx_destroy(kst_ctx* ctx) {
 const char* kst_last_error(const kst_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 long long kst_launch_count(const kst_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int kst_set_gram(kst_ctx* ctx, int mode, int slices) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  if (mode != 0 && mode != 1) return set_err(ctx, KST_ERR_DIMENSION, "gram mode must be 0 or 1");
+  if (mode == 1 && (slices < 3 || slices > 8))
+    return set_err(ctx, KST_ERR_DIMENSION, "int8 Gram needs 3..8 slices, got %d", slices);
+  if (mode == 1 && !kst::ozaki_available())
+    return set_err(ctx, KST_ERR_CUDA, "int8 Gram unavailable: cuBLAS not loadable");
+  ctx->gram_mode = mode;
+  if (mode == 1) ctx->gram_slices = slices;
+  return KST_OK;
+}
+
+double kst_gram_int8_ops(const kst_ctx* ctx) { return ctx ? ctx->last_int8_ops : 0.0; }
+
+int kst_get_gram(const kst_ctx* ctx, int* mode, int* slices) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  if (mode) *mode = ctx->gram_mode;
+  if (slices) *slices = ctx->gram_slices;
+  return KST_OK;
+}
 
 int kst_set_profiling(kst_ctx* ctx, int on) {
   if (!ctx) return KST_ERR_DIMENSION;

@@ -64,6 +64,12 @@ struct kst_ctx {
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
   void* cusolver = nullptr;  // cusolverDnHandle_t, created lazily (heig.cu fallback)
+  void* cublas = nullptr;    // cublasHandle_t for the int8 Gram (gram_ozaki.cu)
+  // K1 engine: 0 = FP64 DMMA tiles (gram.cu), 1 = int8 tensor-core slices
+  // (gram_ozaki.cu) with `gram_slices` 7-bit slices per operand
+  int gram_mode = 0;
+  int gram_slices = 7;
+  double last_int8_ops = 0.0;  // int8 ops issued by the last int8 Gram (bench roofline)
   // instrumentation: kernel launches issued, and per-stage CUDA events of the
   // last kst_pipeline call (recorded only when profiling is on)
   long long launches = 0;
@@ -98,7 +104,9 @@ enum WsSlot {
   WS_PIPE_UB = 14,  // pipeline: temporal basis (lives until detection)
   WS_PIPE_T = 15,   // pipeline: full temporal factor (rank_temporal == q only)
   WS_PIPE_SP = 16,  // pipeline: spatial factor + spatial basis
-  WS_BZ = 17        // eigensolver: split-K partials of B*Z
+  WS_BZ = 17,       // eigensolver: split-K partials of B*Z
+  WS_OZ_SLICES = 18, // int8 Gram: operand slices + column exponents
+  WS_OZ_PROD = 19   // int8 Gram: int32 diagonal products
 };
 
 void* ws_get(kst_ctx* ctx, int slot, size_t bytes);  // may return nullptr on OOM
@@ -186,8 +194,11 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 // ---------------------------------------------------------------- internal API between units
 namespace kst {
-// gram.cu
+// gram.cu (dispatches to gram_ozaki.cu when ctx->gram_mode == 1)
 int scm(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, cudaStream_t st);
+// gram_ozaki.cu
+bool ozaki_available();
+int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s, cudaStream_t st);
 // heig.cu
 struct TopEig {
   int r = 0;

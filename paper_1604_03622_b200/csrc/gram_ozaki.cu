@@ -1,0 +1,267 @@
+// K1 on the int8 tensor cores: Ozaki-style error-free slicing of the FP64
+// Gram S = (1/n) X^T conj(X) (`sample_covariance`, src/lrkron.py:53-78).
+//
+// Each snapshot column a (real and imaginary parts together) is scaled by a
+// power of two 2^-E_a (|x| < 2^E_a) and cut into s signed 7-bit slices
+// (truncation; every remainder is exact in FP64):
+//     x[k,a] = 2^E_a * sum_t sigma_t[k,a] * 2^(-7t) + O(2^(E_a - 7s)).
+// Products of slices are exact in int32, so with the K-stacking trick
+//     G_e = sum_{t+u=e} sigma_t^T sigma_u = [sigma_1..sigma_{e-1}]^T [sigma_{e-1}..sigma_1]
+// one int8 GEMM per diagonal e = 2..s+1 yields every kept pair exactly
+// (|G_e| <= (e-1) K 127^2 < 2^31). Then
+//     Re S = 2^(E_a+E_b)/n * sum_e 2^-7e (GR_e + GI_e)       (GR: Xr.Xr, GI: Xi.Xi)
+//     Im S = 2^(E_a+E_b)/n * sum_e 2^-7e (M_e[a,b] - M_e[b,a]) (M: Xi.Xr)
+// so S is exactly Hermitian with a real diagonal. Dropped pairs (t+u > s+1)
+// and the truncated tail bound the relative error by ~(s+1) 2^(-7s)
+// (s = 6: ~2e-12; s = 7: ~1e-14) of max|x_a| max|x_b| K.
+//
+// The int8 GEMMs are plain library GEMMs (cuBLAS, int8 x int8 -> int32 on
+// the B200 tensor cores, bound with dlopen); slicing and recombination are
+// hand-written kernels. Non-finite columns poison their S entries with NaN so
+// the estimator's finite check raises DataError exactly like the FP64 path.
+#include <cublas_v2.h>  // types only: every cuBLAS entry point is bound with dlsym
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <climits>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kNaNExpo = INT_MIN;
+
+// E_a per column: smallest E with max_k max(|re|, |im|) < 2^E; NaN sentinel
+// for non-finite columns; 0 for all-zero columns (slices are then zero).
+// CTA = 32 columns x 8 row groups (coalesced over columns), smem max-reduce.
+__global__ void colmax_kernel(const cplx* __restrict__ X, int64_t n, int64_t d,
+                              int* __restrict__ expo) {
+  __shared__ double sm[8][33];
+  __shared__ int sb[8][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t a = blockIdx.x * 32 + tx;
+  double m = 0.0;
+  int bad = 0;
+  if (a < d)
+    for (int64_t k = ty; k < n; k += 8) {
+      const cplx v = X[k * d + a];
+      bad |= !isfinite(v.x) || !isfinite(v.y);
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+  sm[ty][tx] = m;
+  sb[ty][tx] = bad;
+  __syncthreads();
+  if (ty == 0 && a < d) {
+    for (int r = 1; r < 8; ++r) {
+      m = fmax(m, sm[r][tx]);
+      bad |= sb[r][tx];
+    }
+    expo[a] = bad ? kNaNExpo : (m > 0.0 ? ilogb(m) + 1 : 0);
+  }
+}
+
+// Slices, column-major per snapshot element a (K blocks of npad contiguous):
+//   RIf[a][2t + c][k] = sigma_{t+1}(part c)[k,a]       (c = 0 real, 1 imag)
+//   RIr[a][2(s-1-t) + c][k] = sigma_{t+1}(part c)[k,a]  (reversed slice order)
+//   If [a][t][k] = sigma_{t+1}(imag),  Rr[a][s-1-t][k] = sigma_{t+1}(real)
+// A prefix of RIf against the matching suffix of RIr pairs (sigma_t, sigma_{e-t})
+// of the same part for every t, so Re = GR_e + GI_e is ONE int8 GEMM per e.
+// 32x32 tiles through smem: X reads coalesced over a, slice writes over k.
+// Padded rows/columns (k >= n, a >= d) are written as zero slices.
+__global__ void slice_kernel(const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d,
+                             int64_t dpad, const int* __restrict__ expo, int s,
+                             int8_t* __restrict__ RIf, int8_t* __restrict__ RIr,
+                             int8_t* __restrict__ If, int8_t* __restrict__ Rr) {
+  __shared__ cplx tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.y * 32, a0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t k = k0 + r, a = a0 + tx;
+    tile[r][tx] = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+  }
+  __syncthreads();
+  for (int c = ty; c < 32; c += 8) {
+    const int64_t a = a0 + c, k = k0 + tx;
+    if (a >= dpad || k >= npad) continue;
+    const int e = a < d ? expo[a] : 0;
+    const cplx v = tile[tx][c];
+    const double sc = (e == kNaNExpo) ? 0.0 : ldexp(1.0, -e);
+    double rr = v.x * sc, ri = v.y * sc;  // |.| < 1
+    const int64_t b2 = a * (int64_t)(2 * s) * npad + k, b1 = a * (int64_t)s * npad + k;
+    for (int t = 0; t < s; ++t) {
+      rr *= 128.0;
+      ri *= 128.0;
+      const double qr = trunc(rr), qi = trunc(ri);
+      rr -= qr;  // exact
+      ri -= qi;
+      RIf[b2 + (int64_t)(2 * t) * npad] = (int8_t)qr;
+      RIf[b2 + (int64_t)(2 * t + 1) * npad] = (int8_t)qi;
+      RIr[b2 + (int64_t)(2 * (s - 1 - t)) * npad] = (int8_t)qr;
+      RIr[b2 + (int64_t)(2 * (s - 1 - t) + 1) * npad] = (int8_t)qi;
+      If[b1 + (int64_t)t * npad] = (int8_t)qi;
+      Rr[b1 + (int64_t)(s - 1 - t) * npad] = (int8_t)qr;
+    }
+  }
+}
+
+// S from the int32 diagonal products (column-major, ld = dpad).
+// CTA per (bi <= bj) pair of 32x32 tiles; writes both S[a][b] and S[b][a].
+__global__ void ozaki_combine_kernel(const int32_t* __restrict__ GRe, const int32_t* __restrict__ GM,
+                                     int64_t dpad, int64_t d, int s, const int* __restrict__ expo,
+                                     double dn, int T, cplx* __restrict__ S) {
+  __shared__ double mt[32][33];  // mt[i][j] = sum_e w_e M_e[b0+i][a0+j]
+  __shared__ cplx vt[32][33];    // vt[i][j] = S[a0+i][b0+j]
+  // upper-triangle tile enumeration
+  const int t = blockIdx.x;
+  double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * t;
+  int bi = (int)floor(((2.0 * T + 1.0) - sqrt(disc)) * 0.5);
+  if (bi < 0) bi = 0;
+  while (bi > 0 && bi * T - bi * (bi - 1) / 2 > t) --bi;
+  while ((bi + 1) * T - (bi + 1) * bi / 2 <= t) ++bi;
+  const int bj = bi + (t - (bi * T - bi * (bi - 1) / 2));
+  const int64_t a0 = (int64_t)bi * 32, b0 = (int64_t)bj * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
+  const size_t plane = (size_t)dpad * dpad;
+  // transposed M block: element (row b0+i, col a0+j) -> column-major index (b0+i) + (a0+j)*dpad
+  // exact weights 2^-7e, accumulated from the smallest term (e = s+1) up
+  const double w0 = ldexp(1.0, -7 * (s + 1));
+  for (int i = ty; i < 32; i += 8) {
+    double acc = 0.0, w = w0;
+    const size_t idx = (size_t)(b0 + tx) + (size_t)(a0 + i) * dpad;  // M[b0+tx][a0+i]
+    for (int e = s + 1; e >= 2; --e, w *= 128.0) acc += (double)GM[(size_t)(e - 2) * plane + idx] * w;
+    mt[tx][i] = acc;  // mt[b-offset][a-offset]
+  }
+  __syncthreads();
+  // (a = a0 + tx, b = b0 + i): column-major G reads coalesced over tx
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t a = a0 + tx, b = b0 + i;
+    const size_t idx = (size_t)a + (size_t)b * dpad;  // G[a][b]
+    double re = 0.0, m_ab = 0.0, w = w0;
+    for (int e = s + 1; e >= 2; --e, w *= 128.0) {
+      re += (double)GRe[(size_t)(e - 2) * plane + idx] * w;
+      m_ab += (double)GM[(size_t)(e - 2) * plane + idx] * w;
+    }
+    const double im = m_ab - mt[i][tx];  // M[a][b] - M[b][a]
+    const int ea = (a < d) ? expo[a] : 0, eb = (b < d) ? expo[b] : 0;
+    cplx v;
+    if (ea == kNaNExpo || eb == kNaNExpo) {
+      v = cmk(NAN, NAN);
+    } else {
+      v = cmk(ldexp(re, ea + eb) / dn, ldexp(im, ea + eb) / dn);
+    }
+    vt[tx][i] = v;
+  }
+  __syncthreads();
+  // row-major S writes, coalesced over the column index
+  for (int r = ty; r < 32; r += 8) {
+    {  // S[a0 + r][b0 + tx] = vt[r][tx]
+      const int64_t a = a0 + r, b = b0 + tx;
+      if (a < d && b < d && (bi != bj || a <= b)) {
+        const cplx v = vt[r][tx];
+        S[a * d + b] = (a == b) ? cmk(v.x, 0.0) : v;
+      }
+    }
+    {  // S[b0 + r][a0 + tx] = conj(vt[tx][r])
+      const int64_t b = b0 + r, a = a0 + tx;
+      if (a < d && b < d && (bi != bj || a < b)) {
+        const cplx v = vt[tx][r];
+        S[b * d + a] = cmk(v.x, -v.y);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- cuBLAS binding
+struct Blas {
+  bool tried = false, ok = false;
+  cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
+  cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
+  cublasStatus_t (*gemm_ex)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                            const void*, const void*, cudaDataType, int, const void*, cudaDataType,
+                            int, const void*, void*, cudaDataType, int, cublasComputeType_t,
+                            cublasGemmAlgo_t) = nullptr;
+};
+Blas g_blas;
+bool load_blas() {
+  if (g_blas.tried) return g_blas.ok;
+  g_blas.tried = true;
+  const char* names[] = {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12"};
+  void* h = nullptr;
+  for (const char* nm : names)
+    if ((h = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+  if (!h) return false;
+  g_blas.create = (decltype(g_blas.create))dlsym(h, "cublasCreate_v2");
+  g_blas.set_stream = (decltype(g_blas.set_stream))dlsym(h, "cublasSetStream_v2");
+  g_blas.gemm_ex = (decltype(g_blas.gemm_ex))dlsym(h, "cublasGemmEx");
+  g_blas.ok = g_blas.create && g_blas.set_stream && g_blas.gemm_ex;
+  return g_blas.ok;
+}
+
+}  // namespace
+
+namespace kst {
+
+bool ozaki_available() { return load_blas(); }
+
+int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s, cudaStream_t st) {
+  if (!load_blas()) return set_err(ctx, KST_ERR_CUDA, "scm_ozaki: cuBLAS not loadable");
+  if (!ctx->cublas) {
+    cublasHandle_t h;
+    if (g_blas.create(&h) != CUBLAS_STATUS_SUCCESS)
+      return set_err(ctx, KST_ERR_CUDA, "cublasCreate failed");
+    ctx->cublas = (void*)h;
+  }
+  cublasHandle_t h = (cublasHandle_t)ctx->cublas;
+  g_blas.set_stream(h, st);
+  const int64_t npad = ((n + 15) / 16) * 16;  // K multiple of 16 (int8 tensor-op alignment)
+  const int64_t dpad = ((d + 31) / 32) * 32;
+  const size_t slice_bytes = (size_t)dpad * s * npad;
+  const size_t plane = (size_t)dpad * dpad;
+  char* sl = (char*)ws_get(ctx, WS_OZ_SLICES, 6 * slice_bytes + sizeof(int) * dpad + 256);
+  int32_t* G = (int32_t*)ws_get(ctx, WS_OZ_PROD, sizeof(int32_t) * 2 * s * plane);
+  if (!sl || !G) return set_err(ctx, KST_ERR_CUDA, "scm_ozaki: workspace");
+  int8_t* RIf = (int8_t*)sl;
+  int8_t* RIr = RIf + 2 * slice_bytes;
+  int8_t* If = RIr + 2 * slice_bytes;
+  int8_t* Rr = If + slice_bytes;
+  int* expo = (int*)(Rr + slice_bytes);
+  int32_t* GRe = G;
+  int32_t* GM = G + (size_t)s * plane;
+
+  colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
+  KST_LAUNCH(ctx);
+  slice_kernel<<<dim3(cdiv(dpad, 32), cdiv(npad, 32)), dim3(32, 8), 0, st>>>(
+      X, n, npad, d, dpad, expo, s, RIf, RIr, If, Rr);
+  KST_LAUNCH(ctx);
+  stage_mark(ctx, 5, st);  // profiling: int8 GEMM span (events 5..6)
+  const int32_t one = 1, zero = 0;
+  const int lda2 = (int)(2 * s * npad), lda1 = (int)(s * npad);
+  for (int e = 2; e <= s + 1; ++e) {
+    int32_t* ore = GRe + (size_t)(e - 2) * plane;
+    int32_t* om = GM + (size_t)(e - 2) * plane;
+    // Re: GR_e + GI_e in one GEMM over the interleaved real/imag slice blocks
+    const int K2 = (int)(2 * (e - 1) * npad);
+    const int64_t off2 = (int64_t)2 * (s - (e - 1)) * npad;  // reversed suffix start
+    cublasStatus_t r1 = g_blas.gemm_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)dpad, (int)dpad, K2, &one,
+                                       RIf, CUDA_R_8I, lda2, RIr + off2, CUDA_R_8I, lda2, &zero, ore,
+                                       CUDA_R_32I, (int)dpad, CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    // M_e = sum_{t+u=e} sigma_t(Xi)^T sigma_u(Xr)
+    const int K1 = (int)((e - 1) * npad);
+    const int64_t off1 = (int64_t)(s - (e - 1)) * npad;
+    cublasStatus_t r3 = g_blas.gemm_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)dpad, (int)dpad, K1, &one,
+                                       If, CUDA_R_8I, lda1, Rr + off1, CUDA_R_8I, lda1, &zero, om,
+                                       CUDA_R_32I, (int)dpad, CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    if (r1 != CUBLAS_STATUS_SUCCESS || r3 != CUBLAS_STATUS_SUCCESS)
+      return set_err(ctx, KST_ERR_CUDA, "cublasGemmEx (int8) failed: %d %d", (int)r1, (int)r3);
+    ctx->launches += 2;
+  }
+  stage_mark(ctx, 6, st);
+  ctx->last_int8_ops = 2.0 * (double)dpad * (double)dpad * (double)npad * 3.0 * s * (s + 1) / 2.0;
+  const int T = (int)(dpad / 32);
+  ozaki_combine_kernel<<<T * (T + 1) / 2, dim3(32, 8), 0, st>>>(GRe, GM, dpad, d, s, expo,
+                                                                (double)n, T, S);
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}
+
+}  // namespace kst

@@ -96,6 +96,21 @@ class KronCovEstimate:
                 f"iterations={self.iterations}, converged={self.converged})")
 
 
+def set_gram_engine(mode="dmma", slices=7, device=None):
+    """Select the sample-covariance engine (K1) for this thread's context:
+    "dmma" (FP64 tensor-core tiles) or "int8" (exact int8 slices on the int8
+    tensor cores, `slices` 7-bit slices per operand)."""
+    c = nat.ctx(device)
+    nat.check(nat.lib().kst_set_gram(c, {"dmma": 0, "int8": 1}[mode], int(slices)), c)
+
+
+def get_gram_engine(device=None):
+    c = nat.ctx(device)
+    m, s = C.c_int(0), C.c_int(0)
+    nat.check(nat.lib().kst_get_gram(c, C.byref(m), C.byref(s)), c)
+    return ("dmma", "int8")[m.value], s.value
+
+
 def _shape(x):
     return tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
 

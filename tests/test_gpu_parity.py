@@ -44,7 +44,11 @@ def test_step_api_matches_reference(name):
     if "scm" in d.files:
         s = scm.matrix
         assert np.array_equal(s, s.conj().T)
-        assert np.linalg.norm(s - d["scm"]) <= 1e-13 * np.linalg.norm(d["scm"])
+        # FP64 DMMA engine: rounding only; int8-slice engine: slice truncation
+        # bound ~(slices+1) 2^(-7 slices) (gram_ozaki.cu)
+        mode, slices = kst.lrkron.get_gram_engine()
+        tol = 1e-13 if mode == "dmma" else 64 * (slices + 1) * 2.0 ** (-7 * slices)
+        assert np.linalg.norm(s - d["scm"]) <= tol * np.linalg.norm(d["scm"])
     est = kst.lr_kron_estimate(scm, int(d["ra"]), int(d["rb"]), tol=float(d["tol"]),
                                max_iter=int(d["max_iter"]))
     assert est.iterations == int(d["iterations"])
@@ -200,3 +204,40 @@ def test_device_tensors_stay_on_device():
     assert img.values.is_cuda
     ref, m0 = d["values"], float(d["m0"])
     assert np.all(np.abs(img.values.cpu().numpy() - ref) <= map_tolerance(ref, m0, 1e-9, 1e-10))
+
+
+@pytest.mark.parametrize("slices", [5, 6, 7, 8])
+def test_int8_gram_engine_error_bound(slices):
+    """The int8 tensor-core Gram against the FP64 DMMA Gram on a cfg-1 scene:
+    exactly Hermitian, real diagonal, relative error within the slice bound."""
+    from paper_1604_03622_b200 import lrkron, scenes
+    cube = scenes.bench_scene(3, 256, 256, seed=17).data[0]
+    snaps = kst.cube_to_snapshots(cube)
+    before = lrkron.get_gram_engine()
+    try:
+        lrkron.set_gram_engine("dmma")
+        ref = kst.sample_covariance(snaps, 3, 256).matrix
+        lrkron.set_gram_engine("int8", slices)
+        s = kst.sample_covariance(snaps, 3, 256).matrix
+    finally:
+        lrkron.set_gram_engine(*before)
+    assert np.array_equal(s, s.conj().T)
+    assert not np.any(np.diagonal(s).imag)
+    dg = np.sqrt(np.outer(ref.diagonal().real, ref.diagonal().real))
+    bound = 64 * (slices + 1) * 2.0 ** (-7 * slices)
+    assert (np.abs(s - ref) / dg).max() <= bound
+    assert np.linalg.norm(s - ref) <= bound * np.linalg.norm(ref)
+
+
+def test_int8_gram_propagates_non_finite_inputs():
+    from paper_1604_03622_b200 import lrkron
+    before = lrkron.get_gram_engine()
+    try:
+        lrkron.set_gram_engine("int8", 6)
+        x = np.ones((8, 6), complex)
+        x[3, 2] = np.nan
+        scm = kst.sample_covariance(x, 2, 3)
+        with pytest.raises(kst.DataError):
+            kst.lr_kron_estimate(scm, 1, 1)
+    finally:
+        lrkron.set_gram_engine(*before)

@@ -106,9 +106,12 @@ __global__ void slice_kernel(const cplx* __restrict__ X, int64_t n, int64_t npad
 
 // S from the int32 diagonal products (column-major, ld = dpad).
 // CTA per (bi <= bj) pair of 32x32 tiles; writes both S[a][b] and S[b][a].
-__global__ void ozaki_combine_kernel(const int32_t* __restrict__ GRe, const int32_t* __restrict__ GM,
-                                     int64_t dpad, int64_t d, int s, const int* __restrict__ expo,
-                                     double dn, int T, cplx* __restrict__ S) {
+// Templated on the slice count so the per-element plane loads are unrolled.
+template <int SS>
+__global__ void __launch_bounds__(256) ozaki_combine_kernel(
+    const int32_t* __restrict__ GRe, const int32_t* __restrict__ GM, int64_t dpad, int64_t d,
+    const int* __restrict__ expo, double dn, int T, cplx* __restrict__ S) {
+  constexpr int s = SS;
   __shared__ double mt[32][33];  // mt[i][j] = sum_e w_e M_e[b0+i][a0+j]
   __shared__ cplx vt[32][33];    // vt[i][j] = S[a0+i][b0+j]
   // upper-triangle tile enumeration
@@ -123,12 +126,22 @@ __global__ void ozaki_combine_kernel(const int32_t* __restrict__ GRe, const int3
   const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
   const size_t plane = (size_t)dpad * dpad;
   // transposed M block: element (row b0+i, col a0+j) -> column-major index (b0+i) + (a0+j)*dpad
-  // exact weights 2^-7e, accumulated from the smallest term (e = s+1) up
+  // exact weights 2^-7e, accumulated from the smallest term (e = s+1) up.
+  // All s loads of an element are issued before any is consumed (unrolled,
+  // predicated), so the kernel streams instead of serialising on latency.
   const double w0 = ldexp(1.0, -7 * (s + 1));
   for (int i = ty; i < 32; i += 8) {
-    double acc = 0.0, w = w0;
     const size_t idx = (size_t)(b0 + tx) + (size_t)(a0 + i) * dpad;  // M[b0+tx][a0+i]
-    for (int e = s + 1; e >= 2; --e, w *= 128.0) acc += (double)GM[(size_t)(e - 2) * plane + idx] * w;
+    int32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = (u < s) ? GM[(size_t)(s - 1 - u) * plane + idx] : 0;
+    double acc = 0.0, w = w0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < s) {
+        acc += (double)v[u] * w;
+        w *= 128.0;
+      }
     mt[tx][i] = acc;  // mt[b-offset][a-offset]
   }
   __syncthreads();
@@ -136,11 +149,20 @@ __global__ void ozaki_combine_kernel(const int32_t* __restrict__ GRe, const int3
   for (int i = ty; i < 32; i += 8) {
     const int64_t a = a0 + tx, b = b0 + i;
     const size_t idx = (size_t)a + (size_t)b * dpad;  // G[a][b]
-    double re = 0.0, m_ab = 0.0, w = w0;
-    for (int e = s + 1; e >= 2; --e, w *= 128.0) {
-      re += (double)GRe[(size_t)(e - 2) * plane + idx] * w;
-      m_ab += (double)GM[(size_t)(e - 2) * plane + idx] * w;
+    int32_t vr[8], vm[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      vr[u] = (u < s) ? GRe[(size_t)(s - 1 - u) * plane + idx] : 0;
+      vm[u] = (u < s) ? GM[(size_t)(s - 1 - u) * plane + idx] : 0;
     }
+    double re = 0.0, m_ab = 0.0, w = w0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < s) {
+        re += (double)vr[u] * w;
+        m_ab += (double)vm[u] * w;
+        w *= 128.0;
+      }
     const double im = m_ab - mt[i][tx];  // M[a][b] - M[b][a]
     const int ea = (a < d) ? expo[a] : 0, eb = (b < d) ? expo[b] : 0;
     cplx v;
@@ -258,8 +280,16 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
   stage_mark(ctx, 6, st);
   ctx->last_int8_ops = 2.0 * (double)dpad * (double)dpad * (double)npad * 3.0 * s * (s + 1) / 2.0;
   const int T = (int)(dpad / 32);
-  ozaki_combine_kernel<<<T * (T + 1) / 2, dim3(32, 8), 0, st>>>(GRe, GM, dpad, d, s, expo,
-                                                                (double)n, T, S);
+  const unsigned nt = T * (T + 1) / 2;
+  const dim3 blk(32, 8);
+  switch (s) {
+    case 3: ozaki_combine_kernel<3><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
+    case 4: ozaki_combine_kernel<4><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
+    case 5: ozaki_combine_kernel<5><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
+    case 6: ozaki_combine_kernel<6><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
+    case 7: ozaki_combine_kernel<7><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
+    default: ozaki_combine_kernel<8><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
+  }
   KST_LAUNCH(ctx);
   return KST_OK;
 }

@@ -224,48 +224,15 @@ __global__ void __launch_bounds__(NT) vstep_kernel(const cplx* __restrict__ S, i
   }
 }
 
-// One CTA: reduce V and |b|^2, spatial truncation, residual, stall test.
-__global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart, int nvx,
-                                                  const double* __restrict__ bpart, int nbp,
-                                                  int P, int ra, double tol, IterState* st,
-                                                  cplx* __restrict__ spatial_out,
-                                                  double* __restrict__ host_out) {
-  extern __shared__ __align__(16) char sm[];
-  __shared__ cplx V[kMaxP * kMaxP];
-  __shared__ cplx Anew[kMaxP * kMaxP];
-  __shared__ double lam[kMaxP];
-  __shared__ double nb2_s;
-  __shared__ int bad_s;
-  __shared__ double red_sh[32];
+// Shared by the streaming and the M-path iterations. On entry V (smem, P x P)
+// = <S4, conj(b)>_{rc} and nb2 = |b|^2 > 0. Performs A = EIG_ra(V / nb2)
+// (src/lrkron.py:207), the expanded-norm residual (src/lrkron.py:210-213) and
+// the stall test (src/lrkron.py:218-221); updates *st. Every thread of the CTA
+// must call it. Returns 0 or KST_ERR_DATA (V not Hermitian), uniformly.
+__device__ int spatial_update(const cplx* V, double nb2, int P, int ra, double tol, IterState* st,
+                              char* sm, cplx* Anew, double* lam, int* bad_s, double* eta_out,
+                              int* conv_out) {
   const int tid = threadIdx.x;
-  {
-    double acc = 0.0;
-    for (int k = tid; k < nbp; k += NT) acc += bpart[k];
-    acc = block_sum<NT>(acc, red_sh);
-    if (tid == 0) nb2_s = acc;
-  }
-  {
-    const int w = tid >> 5, l = tid & 31;
-    for (int k = w; k < 2 * P * P; k += NT / 32) {
-      const int e = k >> 1, ri = k & 1;
-      const int i = e / P, j = e % P;
-      const double v = warp_sum_strided((const double*)vpart + ((size_t)i * nvx * P + j) * 2 + ri,
-                                        nvx, 2 * P);
-      if (l == 0) {
-        if (ri) V[e].y = v;
-        else V[e].x = v;
-      }
-    }
-  }
-  __syncthreads();
-  const double nb2 = nb2_s;
-  if (nb2 == 0.0) {
-    if (tid == 0) {
-      st->status = KST_ERR_DEGENERATE;
-      host_out[0] = KST_ERR_DEGENERATE;
-    }
-    return;
-  }
   // eig_truncate(V / nb2, ra): Hermitian check first (src/linalg.py:68-79)
   if (tid == 0) {
     double f = 0.0, a = 0.0;
@@ -277,15 +244,12 @@ __global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart
         a += cabs2(cmk(x.x - y.x, x.y + y.y));
         if (!isfinite(x.x) || !isfinite(x.y)) a = INFINITY;
       }
-    bad_s = (sqrt(f) > 0 && !(sqrt(a) <= 1e-8 * sqrt(f))) ? 1 : 0;
+    *bad_s = (sqrt(f) > 0 && !(sqrt(a) <= 1e-8 * sqrt(f))) ? 1 : 0;
   }
   __syncthreads();
-  if (bad_s) {
-    if (tid == 0) {
-      st->status = KST_ERR_DATA;
-      host_out[0] = KST_ERR_DATA;
-    }
-    return;
+  if (*bad_s) {
+    if (tid == 0) st->status = KST_ERR_DATA;
+    return KST_ERR_DATA;
   }
   if (ra == P) {
     for (int e = tid; e < P * P; e += NT) {
@@ -338,13 +302,421 @@ __global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart
     st->iteration += 1;
     for (int e = 0; e < P * P; ++e) {
       st->A[e] = Anew[e];
-      spatial_out[e] = Anew[e];
       st->Aconj[e] = cmk(Anew[e].x, -Anew[e].y);
     }
-    host_out[0] = 0;
-    host_out[1] = eta;
-    host_out[2] = conv;
-    host_out[3] = na2;
+    *eta_out = eta;
+    *conv_out = conv;
+  }
+  __syncthreads();
+  return 0;
+}
+
+// One CTA: reduce V and |b|^2, then spatial_update (streaming path).
+__global__ void __launch_bounds__(NT) tail_kernel(const cplx* __restrict__ vpart, int nvx,
+                                                  const double* __restrict__ bpart, int nbp,
+                                                  int P, int ra, double tol, IterState* st,
+                                                  cplx* __restrict__ spatial_out,
+                                                  double* __restrict__ host_out) {
+  extern __shared__ __align__(16) char sm[];
+  __shared__ cplx V[kMaxP * kMaxP];
+  __shared__ cplx Anew[kMaxP * kMaxP];
+  __shared__ double lam[kMaxP];
+  __shared__ double nb2_s, eta_s;
+  __shared__ int bad_s, conv_s;
+  __shared__ double red_sh[32];
+  const int tid = threadIdx.x;
+  {
+    double acc = 0.0;
+    for (int k = tid; k < nbp; k += NT) acc += bpart[k];
+    acc = block_sum<NT>(acc, red_sh);
+    if (tid == 0) nb2_s = acc;
+  }
+  {
+    const int w = tid >> 5, l = tid & 31;
+    for (int k = w; k < 2 * P * P; k += NT / 32) {
+      const int e = k >> 1, ri = k & 1;
+      const int i = e / P, j = e % P;
+      const double v = warp_sum_strided((const double*)vpart + ((size_t)i * nvx * P + j) * 2 + ri,
+                                        nvx, 2 * P);
+      if (l == 0) {
+        if (ri) V[e].y = v;
+        else V[e].x = v;
+      }
+    }
+  }
+  __syncthreads();
+  const double nb2 = nb2_s;
+  if (nb2 == 0.0) {
+    if (tid == 0) {
+      st->status = KST_ERR_DEGENERATE;
+      host_out[0] = KST_ERR_DEGENERATE;
+    }
+    return;
+  }
+  const int rc = spatial_update(V, nb2, P, ra, tol, st, sm, Anew, lam, &bad_s, &eta_s, &conv_s);
+  if (tid == 0) {
+    if (rc) {
+      host_out[0] = rc;
+    } else {
+      for (int e = 0; e < P * P; ++e) spatial_out[e] = Anew[e];
+      host_out[0] = 0;
+      host_out[1] = eta_s;
+      host_out[2] = conv_s;
+      host_out[3] = st->na2;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- M path (P <= 4)
+// b = R^T conj(a) / |a|^2 and V = R conj(b) with R the P^2 x q^2 rearrangement
+// (src/rearrange.py:1-20), so with M = R R^H (P^2 x P^2, Hermitian):
+//   |b|^2 = a^H M a / |a|^4,   V = M a / |a|^2.
+// One pass over S yields M together with |S|_F^2, the block sums A0 and the
+// validation scans; every iteration then runs on the device with no pass
+// over S and no host round trip. The final b needs one last b-step pass.
+constexpr int MG_ROWS = 4;   // rows r per CTA
+constexpr int MG_TILE = 64;  // positions c per smem tile
+
+template <int P>
+struct MDims {
+  static constexpr int U = P * P;
+  static constexpr int E = U * (U + 1) / 2;          // upper-triangle entries of M
+  static constexpr int STRIDE = 4 + 2 * U + 2 * E;   // partial record length
+};
+
+// partial: [fro2, bad, dmin, dmax, A0 re/im (2U), M upper re/im (2E)]
+template <int P>
+__global__ void __launch_bounds__(NT) mgram_kernel(const cplx* __restrict__ S, int q,
+                                                   double* __restrict__ part) {
+  using Dm = MDims<P>;
+  constexpr int U = Dm::U, E = Dm::E;
+  constexpr int G = NT / E > 0 ? NT / E : 1;  // position groups for the M entries
+  __shared__ cplx sv[MG_TILE][U + 1];
+  __shared__ double sh[32];
+  __shared__ int eu[E], ev[E];
+  const int64_t d = (int64_t)P * q;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int k = 0;
+    for (int u = 0; u < U; ++u)
+      for (int v = u; v < U; ++v) {
+        eu[k] = u;
+        ev[k] = v;
+        ++k;
+      }
+  }
+  const int my_e = tid % E, my_g = tid / E;
+  const bool m_active = my_g < G && tid < G * E;
+  double mr = 0.0, mi = 0.0, fro = 0.0, bad = 0.0, dmin = 1e308, dmax = -1e308;
+  double bs[2 * U];
+#pragma unroll
+  for (int u = 0; u < 2 * U; ++u) bs[u] = 0.0;
+  const int r0 = blockIdx.x * MG_ROWS;
+  for (int rr = 0; rr < MG_ROWS && r0 + rr < q; ++rr) {
+    const int r = r0 + rr;
+    for (int c0 = 0; c0 < q; c0 += MG_TILE) {
+      __syncthreads();
+      for (int e = tid; e < MG_TILE * U; e += NT) {
+        const int u = e / MG_TILE, p = e % MG_TILE;  // consecutive threads -> consecutive c
+        const int i = u / P, j = u % P, c = c0 + p;
+        cplx v = cmk(0, 0);
+        if (c < q) {
+          v = S[((int64_t)i * q + r) * d + (int64_t)j * q + c];
+          if (!isfinite(v.x) || !isfinite(v.y)) bad += 1.0;
+          fro = fma(v.x, v.x, fro);
+          fro = fma(v.y, v.y, fro);
+          if (i == j && c == r) {
+            dmin = fmin(dmin, v.x);
+            dmax = fmax(dmax, v.x);
+          }
+        }
+        sv[p][u] = v;
+      }
+      __syncthreads();
+      // block sums: thread u-owner accumulates over the tile in fixed order
+      if (tid < U) {
+        double sr = 0.0, si = 0.0;
+        for (int p = 0; p < MG_TILE; ++p) {
+          sr += sv[p][tid].x;
+          si += sv[p][tid].y;
+        }
+        bs[2 * tid] += sr;
+        bs[2 * tid + 1] += si;
+      }
+      if (m_active) {
+        const int u = eu[my_e], v = ev[my_e];
+        for (int p = my_g; p < MG_TILE; p += G) {
+          const cplx a = sv[p][u], b = sv[p][v];  // M_uv += s_u conj(s_v)
+          mr = fma(a.x, b.x, mr);
+          mr = fma(a.y, b.y, mr);
+          mi = fma(a.y, b.x, mi);
+          mi = fma(-a.x, b.y, mi);
+        }
+      }
+    }
+  }
+  double* out = part + (size_t)blockIdx.x * Dm::STRIDE;
+  fro = block_sum<NT>(fro, sh);
+  bad = block_sum<NT>(bad, sh);
+  // dmin/dmax: fixed-order smem reduction
+  __shared__ double smn[NT], smx[NT];
+  smn[tid] = dmin;
+  smx[tid] = dmax;
+  __syncthreads();
+  if (tid == 0) {
+    double a = 1e308, b = -1e308;
+    for (int k = 0; k < NT; ++k) {
+      a = fmin(a, smn[k]);
+      b = fmax(b, smx[k]);
+    }
+    out[0] = fro;
+    out[1] = bad;
+    out[2] = a;
+    out[3] = b;
+  }
+  if (tid < U) {
+    out[4 + 2 * tid] = bs[2 * tid];
+    out[4 + 2 * tid + 1] = bs[2 * tid + 1];
+  }
+  // M: sum the G position groups of each entry in fixed order
+  __syncthreads();
+  smn[tid] = m_active ? mr : 0.0;
+  smx[tid] = m_active ? mi : 0.0;
+  __syncthreads();
+  if (tid < E) {
+    double ar = 0.0, ai = 0.0;
+    for (int g = 0; g < G; ++g) {
+      ar += smn[g * E + tid];
+      ai += smx[g * E + tid];
+    }
+    out[4 + 2 * U + 2 * tid] = ar;
+    out[4 + 2 * U + 2 * tid + 1] = ai;
+  }
+}
+
+// Register variant for P <= 3: each thread owns positions (r, c) (loads
+// coalesced over c), keeps its s-vector and the whole upper triangle of its
+// partial M in registers, then one fixed-order CTA reduction. Same partial
+// record as mgram_kernel. ~2x fewer instructions than the smem variant and no
+// shared-memory traffic in the hot loop.
+template <int P>
+__global__ void __launch_bounds__(NT, 1) mgram_reg_kernel(const cplx* __restrict__ S, int q,
+                                                          double* __restrict__ part) {
+  using Dm = MDims<P>;
+  constexpr int U = Dm::U, E = Dm::E, R = Dm::STRIDE;
+  __shared__ double red[NT / 32][R];
+  const int64_t d = (int64_t)P * q;
+  const int tid = threadIdx.x;
+  double acc[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) acc[k] = 0.0;
+  acc[2] = 1e308;
+  acc[3] = -1e308;
+  const int r0 = blockIdx.x * MG_ROWS;
+  for (int rr = 0; rr < MG_ROWS && r0 + rr < q; ++rr) {
+    const int r = r0 + rr;
+    for (int c = tid; c < q; c += NT) {
+      cplx sv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = u / P, j = u % P;
+        sv[u] = S[((int64_t)i * q + r) * d + (int64_t)j * q + c];
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const cplx v = sv[u];
+        if (!isfinite(v.x) || !isfinite(v.y)) acc[1] += 1.0;
+        acc[0] = fma(v.x, v.x, acc[0]);
+        acc[0] = fma(v.y, v.y, acc[0]);
+        acc[4 + 2 * u] += v.x;
+        acc[4 + 2 * u + 1] += v.y;
+        if (u / P == u % P && c == r) {
+          acc[2] = fmin(acc[2], v.x);
+          acc[3] = fmax(acc[3], v.x);
+        }
+      }
+      int k = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = u; v < U; ++v, ++k) {
+          const cplx a = sv[u], b = sv[v];  // M_uv += s_u conj(s_v)
+          double& mr = acc[4 + 2 * U + 2 * k];
+          double& mi = acc[4 + 2 * U + 2 * k + 1];
+          mr = fma(a.x, b.x, mr);
+          mr = fma(a.y, b.y, mr);
+          mi = fma(a.y, b.x, mi);
+          mi = fma(-a.x, b.y, mi);
+        }
+    }
+  }
+  // fixed-order reduction: warp shuffle tree, then warps in order
+  const int w = tid >> 5, l = tid & 31;
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    double v = acc[k];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (k == 2) ? fmin(v, x) : (k == 3) ? fmax(v, x) : v + x;
+    }
+    if (l == 0) red[w][k] = v;
+  }
+  __syncthreads();
+  double* out = part + (size_t)blockIdx.x * R;
+  for (int k = tid; k < R; k += NT) {
+    double v = red[0][k];
+    for (int ww = 1; ww < NT / 32; ++ww)
+      v = (k == 2) ? fmin(v, red[ww][k]) : (k == 3) ? fmax(v, red[ww][k]) : v + red[ww][k];
+    out[k] = v;
+  }
+  (void)E;
+}
+
+// Reduce mgram partials (fixed order) and run ALL iterations in one CTA.
+// Outputs: spatial (final A), residuals[max_iter], info[0..3] = {status,
+// iterations, converged, pad}, host_diag[0..4] = {bad, dmin, dmax, fro, na2_0};
+// st->Aconj / st->na2 are left holding the A that produced the final b.
+template <int P>
+__global__ void __launch_bounds__(NT) m_iterate_kernel(const double* __restrict__ part, int nblk,
+                                                       int q, int ra, double tol, int max_iter,
+                                                       IterState* st, cplx* __restrict__ spatial_out,
+                                                       double* __restrict__ residuals,
+                                                       double* __restrict__ info,
+                                                       double* __restrict__ host_diag) {
+  using Dm = MDims<P>;
+  constexpr int U = Dm::U, E = Dm::E;
+  extern __shared__ __align__(16) char sm[];
+  __shared__ double red[4 + 2 * U + 2 * E];
+  __shared__ cplx M[U * U];
+  __shared__ cplx V[kMaxP * kMaxP];
+  __shared__ cplx Anew[kMaxP * kMaxP];
+  __shared__ cplx Ma[U];
+  __shared__ double lam[kMaxP];
+  __shared__ double eta_s, scal[4];
+  __shared__ int bad_s, conv_s, stop_s;
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+  for (int k = w; k < Dm::STRIDE; k += NT / 32) {
+    double v;
+    if (k == 2 || k == 3) {
+      double m = (k == 2) ? 1e308 : -1e308;
+      for (int b = l; b < nblk; b += 32)
+        m = (k == 2) ? fmin(m, part[(size_t)b * Dm::STRIDE + k]) : fmax(m, part[(size_t)b * Dm::STRIDE + k]);
+      v = (k == 2) ? warp_min(m) : warp_max(m);
+    } else {
+      v = warp_sum_strided(part + k, nblk, Dm::STRIDE);
+    }
+    if (l == 0) red[k] = v;
+  }
+  __syncthreads();
+  for (int k = tid; k < E; k += NT) {
+    // unpack the upper triangle into the full Hermitian M
+    int u = 0, rem = k;
+    while (rem >= U - u) {
+      rem -= U - u;
+      ++u;
+    }
+    const int v = u + rem;
+    const cplx m = cmk(red[4 + 2 * U + 2 * k], red[4 + 2 * U + 2 * k + 1]);
+    M[u * U + v] = m;
+    M[v * U + u] = cconj(m);
+  }
+  if (tid == 0) {
+    const double qq = (double)q * (double)q;
+    double na2 = 0.0;
+    for (int e = 0; e < U; ++e) {
+      const cplx a = cmk(red[4 + 2 * e] / qq, red[5 + 2 * e] / qq);
+      st->A[e] = a;
+      st->Aconj[e] = cconj(a);
+      na2 += cabs2(a);
+    }
+    st->fro2 = red[0];
+    st->fro = sqrt(red[0]);
+    st->na2 = na2;
+    st->eta_prev = INFINITY;
+    st->status = 0;
+    st->converged = 0;
+    st->iteration = 0;
+    host_diag[0] = red[1];
+    host_diag[1] = red[2];
+    host_diag[2] = red[3];
+    host_diag[3] = st->fro;
+    host_diag[4] = na2;
+    stop_s = (red[1] > 0.0 || red[0] == 0.0) ? 1 : 0;  // host handles bad input / zero S
+  }
+  __syncthreads();
+  int status = 0, iters = 0, conv = 0;
+  if (!stop_s) {
+    for (int it = 0; it < max_iter; ++it) {
+      if (tid == 0) {
+        scal[0] = st->na2;
+        stop_s = 0;
+      }
+      __syncthreads();
+      const double na2 = scal[0];
+      if (na2 == 0.0) {
+        status = 4;  // spatial iterate collapsed (reference raises at iteration start)
+        break;
+      }
+      // Ma = M a ; nb2 = Re(a^H M a) / na2^2 ; V = Ma / na2
+      for (int u = tid; u < U; u += NT) {
+        cplx acc = cmk(0, 0);
+        for (int v = 0; v < U; ++v) cfma(acc, M[u * U + v], st->A[v]);
+        Ma[u] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double q2 = 0.0;
+        for (int u = 0; u < U; ++u) q2 += st->A[u].x * Ma[u].x + st->A[u].y * Ma[u].y;
+        scal[1] = q2 / (na2 * na2);
+        for (int u = 0; u < U; ++u) V[u] = cmk(Ma[u].x / na2, Ma[u].y / na2);
+        // the A that produces this iteration's b (kept for the final b-step)
+        scal[2] = na2;
+      }
+      __syncthreads();
+      const double nb2 = scal[1];
+      ++iters;
+      if (nb2 == 0.0) {
+        status = KST_ERR_DEGENERATE;
+        break;
+      }
+      // keep the b-producing A for the final b-step before spatial_update overwrites it
+      __shared__ cplx Aprev[kMaxP * kMaxP];
+      for (int e = tid; e < U; e += NT) Aprev[e] = st->A[e];
+      __syncthreads();
+      const int rc = spatial_update(V, nb2, P, ra, tol, st, sm, Anew, lam, &bad_s, &eta_s, &conv_s);
+      if (rc) {
+        status = rc;
+        break;
+      }
+      if (tid == 0) residuals[it] = eta_s;
+      const int c_now = conv_s;
+      __syncthreads();
+      if (c_now) {
+        conv = 1;
+        // leave Aconj / na2 describing the b-producing A
+        if (tid == 0) {
+          for (int e = 0; e < U; ++e) {
+            spatial_out[e] = st->A[e];
+            st->Aconj[e] = cconj(Aprev[e]);
+          }
+          st->na2 = scal[2];
+        }
+        break;
+      }
+      if (it == max_iter - 1 && tid == 0) {
+        for (int e = 0; e < U; ++e) {
+          spatial_out[e] = st->A[e];
+          st->Aconj[e] = cconj(Aprev[e]);
+        }
+        st->na2 = scal[2];
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    info[0] = status;
+    info[1] = iters;
+    info[2] = conv;
   }
 }
 
@@ -375,14 +747,58 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
       std::max(sizeof(double) * stat_stride * p * nbx,
                sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64));
   cplx* b = (cplx*)ws_get(ctx, WS_B, sizeof(cplx) * (size_t)q * q);
-  double* hbuf = (double*)pinned_get(ctx, 64 * sizeof(double));
+  // one pinned staging buffer: [0, 64) small scalars, [64, ...) M-path residuals
+  double* hbuf = (double*)pinned_get(ctx, sizeof(double) * (64 + std::max(max_iter, 1) + 32));
   if (!small || !part || !b || !hbuf) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");
   IterState* state = (IterState*)small;
 
-  KST_DISPATCH_P(p, (stats_kernel<PP><<<dim3(nbx, p), NT, 0, st>>>(S, q, part)));
-  KST_LAUNCH(ctx);
-  init_kernel<<<1, NT, 0, st>>>(part, nbx, p, q, state, (double*)(small + sizeof(IterState)));
-  KST_LAUNCH(ctx);
+  // M path: small P, valid ranks, no per-iteration b copies requested
+  static const bool mpath_env = !(getenv("KST_LRKRON_MPATH") && atoi(getenv("KST_LRKRON_MPATH")) == 0);
+  const bool mpath = mpath_env && p <= 4 && !iter_b && !iter_spatial && ra >= 1 && ra <= p &&
+                     rb >= 1 && rb <= q && max_iter >= 1;
+  double* mres = nullptr;
+  double* minfo = nullptr;
+  if (mpath) {
+    const int nblk = (q + MG_ROWS - 1) / MG_ROWS;
+    size_t rec = 0;
+    KST_DISPATCH_P(p, (rec = MDims<PP>::STRIDE));
+    double* mpart = (double*)ws_get(ctx, WS_PART, sizeof(double) * rec * nblk + 64);
+    double* dres = (double*)ws_get(ctx, WS_VALS, sizeof(double) * (max_iter + 8));
+    mres = hbuf ? hbuf + 64 : nullptr;
+    if (!mpart || !dres || !mres) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");
+    minfo = dres + max_iter;
+    const size_t jsm = jac_smem_bytes(p);
+    switch (p) {
+      case 1:
+        mgram_reg_kernel<1><<<nblk, NT, 0, st>>>(S, q, mpart);
+        m_iterate_kernel<1><<<1, NT, jsm, st>>>(mpart, nblk, q, ra, tol, max_iter, state, spatial,
+                                                 dres, minfo, (double*)(small + sizeof(IterState)));
+        break;
+      case 2:
+        mgram_reg_kernel<2><<<nblk, NT, 0, st>>>(S, q, mpart);
+        m_iterate_kernel<2><<<1, NT, jsm, st>>>(mpart, nblk, q, ra, tol, max_iter, state, spatial,
+                                                 dres, minfo, (double*)(small + sizeof(IterState)));
+        break;
+      case 3:
+        mgram_reg_kernel<3><<<nblk, NT, 0, st>>>(S, q, mpart);
+        m_iterate_kernel<3><<<1, NT, jsm, st>>>(mpart, nblk, q, ra, tol, max_iter, state, spatial,
+                                                 dres, minfo, (double*)(small + sizeof(IterState)));
+        break;
+      default:
+        mgram_kernel<4><<<nblk, NT, 0, st>>>(S, q, mpart);
+        m_iterate_kernel<4><<<1, NT, jsm, st>>>(mpart, nblk, q, ra, tol, max_iter, state, spatial,
+                                                 dres, minfo, (double*)(small + sizeof(IterState)));
+        break;
+    }
+    ctx->launches += 1;  // + 1 in KST_LAUNCH: mgram + m_iterate
+    KST_LAUNCH(ctx);
+    KST_CUDA(ctx, cudaMemcpyAsync(mres, dres, sizeof(double) * (max_iter + 3), cudaMemcpyDeviceToHost, st));
+  } else {
+    KST_DISPATCH_P(p, (stats_kernel<PP><<<dim3(nbx, p), NT, 0, st>>>(S, q, part)));
+    KST_LAUNCH(ctx);
+    init_kernel<<<1, NT, 0, st>>>(part, nbx, p, q, state, (double*)(small + sizeof(IterState)));
+    KST_LAUNCH(ctx);
+  }
   KST_CUDA(ctx, cudaMemcpyAsync(hbuf, small + sizeof(IterState), 5 * sizeof(double),
                                 cudaMemcpyDeviceToHost, st));
   KST_CUDA(ctx, cudaStreamSynchronize(st));
@@ -423,7 +839,22 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   double* hout = (double*)(small + sizeof(IterState) + 64);
   const size_t tail_smem = jac_smem_bytes(p);
   int iters = 0, conv = 0;
-  for (int it = 0; it < max_iter; ++it) {
+  if (mpath) {
+    // all iterations already ran on the device (m_iterate_kernel)
+    const int status = (int)mres[max_iter];
+    iters = (int)mres[max_iter + 1];
+    conv = (int)mres[max_iter + 2];
+    if (status == 4) return set_err(ctx, KST_ERR_DEGENERATE, "spatial iterate collapsed to zero");
+    if (status == KST_ERR_DEGENERATE)
+      return set_err(ctx, KST_ERR_DEGENERATE, "temporal iterate collapsed to zero");
+    if (status == KST_ERR_DATA)
+      return set_err(ctx, KST_ERR_DATA, "matrix deviates from Hermitian beyond tolerance");
+    for (int it = 0; it < iters; ++it) fit->residuals.push_back(mres[it]);
+    // final b from the A that entered the last iteration (st->Aconj / st->na2)
+    KST_DISPATCH_P(p, (bstep_kernel<PP><<<dim3(nbb, q), NT, 0, st>>>(S, q, state, b, bpart)));
+    KST_LAUNCH(ctx);
+  }
+  for (int it = 0; it < max_iter && !mpath; ++it) {
     if (na2 == 0.0) return set_err(ctx, KST_ERR_DEGENERATE, "spatial iterate collapsed to zero");
     ++iters;
     KST_DISPATCH_P(p, (bstep_kernel<PP><<<dim3(nbb, q), NT, 0, st>>>(S, q, state, b, bpart)));

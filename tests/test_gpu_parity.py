@@ -241,3 +241,23 @@ def test_int8_gram_propagates_non_finite_inputs():
             kst.lr_kron_estimate(scm, 1, 1)
     finally:
         lrkron.set_gram_engine(*before)
+
+
+def test_frame_stream_overlap_matches_single_frames():
+    from paper_1604_03622_b200 import scenes
+    from paper_1604_03622_b200.pipeline import FrameStream
+    cubes = [scenes.bench_scene(3, 64, 80, seed=200 + i, movers=2).data[0] for i in range(4)]
+    pinned = [torch.from_numpy(c).pin_memory() for c in cubes]
+    fs = FrameStream(cubes[0].shape, 0, 1, 3)
+    got = []
+    for c in pinned:
+        r = fs.submit(c)
+        if r is not None:
+            r[1].synchronize()
+            got.append(r[0].numpy().copy())
+    r = fs.flush()
+    r[1].synchronize()
+    got.append(r[0].numpy().copy())
+    for c, g in zip(cubes, got):
+        want, _ = kst.process_frame(c, 1, 3)
+        assert np.array_equal(g, want)

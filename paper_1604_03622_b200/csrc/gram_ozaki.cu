@@ -202,6 +202,11 @@ struct Blas {
                             const void*, const void*, cudaDataType, int, const void*, cudaDataType,
                             int, const void*, void*, cudaDataType, int, cublasComputeType_t,
                             cublasGemmAlgo_t) = nullptr;
+  cublasStatus_t (*gemm_batched_ex)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int,
+                                    int, const void*, const void* const[], cudaDataType, int,
+                                    const void* const[], cudaDataType, int, const void*,
+                                    void* const[], cudaDataType, int, int, cublasComputeType_t,
+                                    cublasGemmAlgo_t) = nullptr;
 };
 Blas g_blas;
 bool load_blas() {
@@ -215,7 +220,8 @@ bool load_blas() {
   g_blas.create = (decltype(g_blas.create))dlsym(h, "cublasCreate_v2");
   g_blas.set_stream = (decltype(g_blas.set_stream))dlsym(h, "cublasSetStream_v2");
   g_blas.gemm_ex = (decltype(g_blas.gemm_ex))dlsym(h, "cublasGemmEx");
-  g_blas.ok = g_blas.create && g_blas.set_stream && g_blas.gemm_ex;
+  g_blas.gemm_batched_ex = (decltype(g_blas.gemm_batched_ex))dlsym(h, "cublasGemmBatchedEx");
+  g_blas.ok = g_blas.create && g_blas.set_stream && g_blas.gemm_ex && g_blas.gemm_batched_ex;
   return g_blas.ok;
 }
 
@@ -236,10 +242,17 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
   cublasHandle_t h = (cublasHandle_t)ctx->cublas;
   g_blas.set_stream(h, st);
   const int64_t npad = ((n + 15) / 16) * 16;  // K multiple of 16 (int8 tensor-op alignment)
-  const int64_t dpad = ((d + 31) / 32) * 32;
+  // Re = GR + GI is symmetric: for large d only the NB(NB+1)/2 upper blocks of
+  // an NB x NB block grid are multiplied (one batched GEMM per diagonal e).
+  constexpr int NB = 4;
+  const bool blocked = d >= 1024;
+  const int64_t dpad = blocked ? ((d + 32 * NB - 1) / (32 * NB)) * (32 * NB) : ((d + 31) / 32) * 32;
+  const int64_t bsz = dpad / NB;
+  constexpr int NBLK = NB * (NB + 1) / 2;
   const size_t slice_bytes = (size_t)dpad * s * npad;
   const size_t plane = (size_t)dpad * dpad;
-  char* sl = (char*)ws_get(ctx, WS_OZ_SLICES, 6 * slice_bytes + sizeof(int) * dpad + 256);
+  char* sl = (char*)ws_get(ctx, WS_OZ_SLICES, 6 * slice_bytes + sizeof(int) * dpad +
+                                                   sizeof(void*) * 3 * NBLK * 8 + 512);
   int32_t* G = (int32_t*)ws_get(ctx, WS_OZ_PROD, sizeof(int32_t) * 2 * s * plane);
   if (!sl || !G) return set_err(ctx, KST_ERR_CUDA, "scm_ozaki: workspace");
   int8_t* RIf = (int8_t*)sl;
@@ -247,8 +260,32 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
   int8_t* If = RIr + 2 * slice_bytes;
   int8_t* Rr = If + slice_bytes;
   int* expo = (int*)(Rr + slice_bytes);
+  void** dptr = (void**)(((uintptr_t)(expo + dpad) + 255) & ~(uintptr_t)255);  // batched pointers
   int32_t* GRe = G;
   int32_t* GM = G + (size_t)s * plane;
+  if (blocked) {
+    // pointer arrays for every (e, upper block): A, B, C
+    void** hp = (void**)pinned_get(ctx, sizeof(void*) * 6 * NBLK * 8);
+    if (!hp) return set_err(ctx, KST_ERR_CUDA, "scm_ozaki: pinned staging");
+    const int lda2 = (int)(2 * s * npad);
+    for (int e = 2; e <= s + 1; ++e) {
+      const int64_t off2 = (int64_t)2 * (s - (e - 1)) * npad;
+      int k = 0;
+      for (int I = 0; I < NB; ++I)
+        for (int J = I; J < NB; ++J, ++k) {
+          void** row = hp + ((size_t)(e - 2) * NBLK + k) * 3;
+          row[0] = (void*)(RIf + (size_t)I * bsz * lda2);
+          row[1] = (void*)(RIr + off2 + (size_t)J * bsz * lda2);
+          row[2] = (void*)(GRe + (size_t)(e - 2) * plane + I * bsz + (size_t)J * bsz * dpad);
+        }
+    }
+    // de-interleave into A[], B[], C[] arrays per e on the host buffer tail
+    void** ha = hp + 3 * NBLK * s;
+    for (int e = 0; e < s; ++e)
+      for (int k = 0; k < NBLK; ++k)
+        for (int c = 0; c < 3; ++c) ha[((size_t)c * s + e) * NBLK + k] = hp[((size_t)e * NBLK + k) * 3 + c];
+    KST_CUDA(ctx, cudaMemcpyAsync(dptr, ha, sizeof(void*) * 3 * NBLK * s, cudaMemcpyHostToDevice, st));
+  }
 
   colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
   KST_LAUNCH(ctx);
@@ -264,9 +301,20 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
     // Re: GR_e + GI_e in one GEMM over the interleaved real/imag slice blocks
     const int K2 = (int)(2 * (e - 1) * npad);
     const int64_t off2 = (int64_t)2 * (s - (e - 1)) * npad;  // reversed suffix start
-    cublasStatus_t r1 = g_blas.gemm_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)dpad, (int)dpad, K2, &one,
-                                       RIf, CUDA_R_8I, lda2, RIr + off2, CUDA_R_8I, lda2, &zero, ore,
-                                       CUDA_R_32I, (int)dpad, CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    cublasStatus_t r1;
+    if (blocked) {
+      void** A = dptr + (size_t)(0 * s + (e - 2)) * NBLK;
+      void** B = dptr + (size_t)(1 * s + (e - 2)) * NBLK;
+      void** Cc = dptr + (size_t)(2 * s + (e - 2)) * NBLK;
+      r1 = g_blas.gemm_batched_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)bsz, (int)bsz, K2, &one,
+                                  (const void* const*)A, CUDA_R_8I, lda2, (const void* const*)B,
+                                  CUDA_R_8I, lda2, &zero, Cc, CUDA_R_32I, (int)dpad, NBLK,
+                                  CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    } else {
+      r1 = g_blas.gemm_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)dpad, (int)dpad, K2, &one, RIf,
+                          CUDA_R_8I, lda2, RIr + off2, CUDA_R_8I, lda2, &zero, ore, CUDA_R_32I,
+                          (int)dpad, CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    }
     // M_e = sum_{t+u=e} sigma_t(Xi)^T sigma_u(Xr)
     const int K1 = (int)((e - 1) * npad);
     const int64_t off1 = (int64_t)(s - (e - 1)) * npad;
@@ -278,7 +326,11 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
     ctx->launches += 2;
   }
   stage_mark(ctx, 6, st);
-  ctx->last_int8_ops = 2.0 * (double)dpad * (double)dpad * (double)npad * 3.0 * s * (s + 1) / 2.0;
+  {
+    const double re_frac = blocked ? (double)NBLK / (NB * NB) : 1.0;  // Re: upper blocks only
+    const double k_re = 2.0 * npad * s * (s + 1) / 2.0, k_m = (double)npad * s * (s + 1) / 2.0;
+    ctx->last_int8_ops = 2.0 * (double)dpad * (double)dpad * (re_frac * k_re + k_m);
+  }
   const int T = (int)(dpad / 32);
   const unsigned nt = T * (T + 1) / 2;
   const dim3 blk(32, 8);

@@ -27,9 +27,7 @@ __global__ void jacobi_eig_kernel(const cplx* __restrict__ M, int ldm, int n, do
                                   int ldv) {
   extern __shared__ __align__(16) char sm[];
   JacSmem j = jac_carve(sm, n);
-  jac_load_sym(j, M, ldm, n, div);
-  jac_sweeps(j, n);
-  jac_finish(j, n);
+  jac_solve(j, M, ldm, n, div);
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, k = e % n;
     vectors[(size_t)i * ldv + k] = j.V[i * j.ld + j.order[k]];
@@ -335,7 +333,7 @@ __global__ void finalize_top_kernel(const cplx* __restrict__ Z, int n, int s, in
   __shared__ int order[32];
   __shared__ double phr[32], phi[32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  for (int k = w; k < s; k += 8) {
+  for (int k = w; k < s; k += (int)(blockDim.x >> 5)) {
     double bm = -1.0;
     int bi = 0;
     for (int i = l; i < n; i += 32) {
@@ -537,28 +535,21 @@ __global__ void __launch_bounds__(256) k4_small_kernel(const cplx* __restrict__ 
   cplx* Q = G + s * s;
   cplx* T = Q + s * s;
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
-  const int nw = blockDim.x >> 5;
-  // fixed-order reduction of the partials
-  for (int k = w; k < 4 * s * s; k += nw) {
-    const int comp = k & 1, e = k >> 1;  // e indexes [which][a][b]
-    double acc = 0.0;
-    for (int b = l; b < nblk; b += 32) {
-      const cplx v = partial[(size_t)b * 2 * s * s + e];
-      acc += comp ? v.y : v.x;
-    }
-    acc = warp_sum(acc);
-    if (l == 0) {
-      cplx* dst = e < s * s ? &H[e] : &G[e - s * s];
-      if (comp) dst->y = acc;
-      else dst->x = acc;
-    }
+  (void)w;
+  (void)l;
+  // fixed-order reduction of the partials: one thread per complex entry, the
+  // nblk loads of an entry are independent and issued back to back
+  for (int e = tid; e < 2 * s * s; e += blockDim.x) {
+    cplx acc = cmk(0, 0);
+#pragma unroll 8
+    for (int b = 0; b < nblk; ++b) acc = cadd(acc, partial[(size_t)b * 2 * s * s + e]);
+    if (e < s * s) H[e] = acc;
+    else G[e - s * s] = acc;
   }
   __syncthreads();
   JacSmem j = jac_carve(sm, s);
   if (mode == 0) {
-    jac_load_sym(j, H, s, s, 1.0);
-    jac_sweeps(j, s);
-    jac_finish(j, s);
+    jac_solve(j, H, s, s, 1.0);
     for (int e = tid; e < s * s; e += blockDim.x) {
       const int i = e / s, k = e % s;
       Q[e] = j.V[i * j.ld + j.order[k]];
@@ -650,9 +641,7 @@ __global__ void __launch_bounds__(256) k4_small_kernel(const cplx* __restrict__ 
       return;
     }
   }
-  jac_load_sym(j, G, s, s, 1.0);
-  jac_sweeps(j, s);
-  jac_finish(j, s);
+  jac_solve(j, G, s, s, 1.0);
   // C = Q D V S^-1. Nearly dependent directions are NOT dropped: their tiny
   // singular values are floored, so they come back as amplified rounding
   // noise -- fresh trial directions -- and the next pass orthonormalises them.
@@ -959,7 +948,7 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   auto step = [&](const cplx* Zc, const cplx* Y1, const cplx* Y2c, int mode) -> int {
     k4_gram_kernel<<<nblk, 256, 0, st>>>(Zc, Y1, Y2c, n, s, partial);
     KST_LAUNCH(ctx);
-    k4_small_kernel<<<1, 64, small_smem, st>>>(partial, nblk, s, mode, Cm, Qm, theta, info);
+    k4_small_kernel<<<1, 128, small_smem, st>>>(partial, nblk, s, mode, Cm, Qm, theta, info);
     KST_LAUNCH(ctx);
     k4_update_kernel<<<nup, dim3(32, 8), 0, st>>>(Y1, Y2c, Zc, n, s, r, mode, Cm, Qm, theta, Zn,
                                                    X, res_part);
@@ -971,6 +960,15 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   // construction; B e_i is the i-th column, rich in the dominant directions)
   unit_start_kernel<<<1, 256, 0, st>>>(M, n, s, Z);
   KST_LAUNCH(ctx);
+  // Warm-up without Rayleigh-Ritz (Ritz pairs of the start block are useless):
+  // Z <- orth(B^4 Z0), two orthonormalisation passes (SVQB when the block is
+  // ill-conditioned, Cholesky-QR once it is not).
+  KST_TRY(bz(ctx, M, n, Z, s, Y, st));
+  KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
+  KST_TRY(bz(ctx, M, n, Y2, s, Y, st));
+  KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
+  KST_TRY(step(Z, Z, Y2, 1));
+  KST_TRY(step(Z, Z, Z, 1));
 
   bool converged = false;
   double prev_worst = 1e300;
@@ -1020,7 +1018,7 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     if (!converged && path != 2) KST_TRY(step(Z, Z, Z, 1));
   }
   if (!converged) return heig_top_cusolver(ctx, M, n, r, values_host, vectors, st);
-  finalize_top_kernel<<<1, 256, 0, st>>>(X, n, s, r, theta, vout, vectors);
+  finalize_top_kernel<<<1, 1024, 0, st>>>(X, n, s, r, theta, vout, vectors);
   KST_LAUNCH(ctx);
   if (values_host) {
     KST_CUDA(ctx, cudaMemcpyAsync(values_host, vout, sizeof(double) * r, cudaMemcpyDeviceToHost, st));

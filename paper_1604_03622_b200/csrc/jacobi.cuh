@@ -205,6 +205,167 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- warp Jacobi
+// Register-resident cyclic Jacobi for n <= N (N in {4, 8, 16}) run by ONE warp:
+// lane l < N owns column l of A and of V; the N-1 rounds of a sweep are
+// unrolled at compile time so every row index is static; partner columns and
+// the rotation parameters move by warp shuffles (no shared memory, no block
+// barriers). Same rotation formulas, thresholds and exact 2x2 diagonal
+// update as jac_sweeps. Matrices with n < N are zero-padded; the padded
+// indices never rotate (their off-diagonals are exact zeros).
+// Reads (M/div + (M/div)^H)/2 (M row-major, leading dim ldm); writes j.V and
+// j.val for the first n indices. Call from warp 0 only; follow with
+// __syncthreads() and jac_finish(j, n).
+template <int N>
+__device__ inline void warp_jacobi(JacSmem& j, const cplx* M, int ldm, int n, double div) {
+  const int l = threadIdx.x & 31;
+  cplx a[N], v[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    cplx x = cmk(0, 0);
+    if (l < n && k < n) {
+      const cplx m1 = M[(size_t)k * ldm + l], m2 = M[(size_t)l * ldm + k];
+      x = cmk(((m1.x / div) + (m2.x / div)) / 2.0, ((m1.y / div) - (m2.y / div)) / 2.0);
+    }
+    a[k] = x;
+    v[k] = cmk((k == l) ? 1.0 : 0.0, 0.0);
+  }
+  // Frobenius norm (absolute rotation floor), identical in every lane
+  double f = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) f += cabs2(a[k]);
+  f = warp_sum(f);
+  const double fro2 = f;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int rotated = 0;
+#pragma unroll
+    for (int round = 0; round < N - 1; ++round) {
+      // partner of lane l in this round (tournament, player 0 fixed)
+      int m;
+      if (l == 0) m = 1 + round % (N - 1);
+      else if (l == 1 + round % (N - 1)) m = 0;
+      else {
+        const int pos = (l - 1 - round + 2 * (N - 1)) % (N - 1);  // circle position of l
+        const int mpos = (N - 1 - pos) % (N - 1);                   // opposite position
+        m = 1 + (mpos + round) % (N - 1);
+      }
+      if (l >= N) m = l;
+      const bool is_p = l < m;
+      // own diagonal a[l] and the cross element a[m] (row m of own column)
+      cplx dl = cmk(0, 0), xm = cmk(0, 0);
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        if (k == l) dl = a[k];
+        if (k == m) xm = a[k];
+      }
+      const double dm = __shfl_sync(0xffffffffu, dl.x, m & 31);
+      const double app = is_p ? dl.x : dm, aqq = is_p ? dm : dl.x;
+      const cplx apq = is_p ? cconj(xm) : xm;  // A[p][q]
+      double c = 1.0, s = 0.0, ec = 1.0, es = 0.0, tr = 0.0;
+      const double r2 = apq.x * apq.x + apq.y * apq.y;
+      const double thr2 = fmax(4.84e-32 * fabs(app) * fabs(aqq), 1e-30 * fro2);
+      if (l < N && m != l && r2 > thr2) {
+        const double rinv = rsqrt(r2);
+        const double r = r2 * rinv;
+        ec = apq.x * rinv;
+        es = apq.y * rinv;
+        const double tau = (aqq - app) * (0.5 * rinv);
+        const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+        c = rsqrt(fma(t, t, 1.0));
+        s = t * c;
+        tr = t * r;
+      }
+      {  // both lanes of a pair use the p-lane's parameters (exactly one rotation)
+        const int src = is_p ? l : (m & 31);
+        c = __shfl_sync(0xffffffffu, c, src);
+        s = __shfl_sync(0xffffffffu, s, src);
+        ec = __shfl_sync(0xffffffffu, ec, src);
+        es = __shfl_sync(0xffffffffu, es, src);
+        tr = __shfl_sync(0xffffffffu, tr, src);
+        if (s != 0.0) rotated = 1;
+      }
+      // column update with the partner's column (A and V)
+      const cplx emi = cmk(ec, -es);  // e^{-i phi}
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        const double yx = __shfl_sync(0xffffffffu, a[k].x, m & 31);
+        const double yy = __shfl_sync(0xffffffffu, a[k].y, m & 31);
+        const double vx = __shfl_sync(0xffffffffu, v[k].x, m & 31);
+        const double vy = __shfl_sync(0xffffffffu, v[k].y, m & 31);
+        if (s != 0.0) {
+          if (is_p) {  // col_p' = c col_p - s e^{-i phi} col_q
+            const cplx wq = cmul(emi, cmk(yx, yy)), wv = cmul(emi, cmk(vx, vy));
+            a[k] = cmk(c * a[k].x - s * wq.x, c * a[k].y - s * wq.y);
+            v[k] = cmk(c * v[k].x - s * wv.x, c * v[k].y - s * wv.y);
+          } else {     // col_q' = s col_p + c e^{-i phi} col_q
+            const cplx wq = cmul(emi, a[k]), wv = cmul(emi, v[k]);
+            a[k] = cmk(s * yx + c * wq.x, s * yy + c * wq.y);
+            v[k] = cmk(s * vx + c * wv.x, s * vy + c * wv.y);
+          }
+        }
+      }
+      // row update: every pair's rows (p, q) in every owned column
+#pragma unroll
+      for (int k2 = 0; k2 < N / 2; ++k2) {
+        int pa, pb;  // the pair k2 of this round (compile-time indices)
+        if (k2 == 0) {
+          pa = 0;
+          pb = 1 + round % (N - 1);
+        } else {
+          pa = 1 + (round + k2) % (N - 1);
+          pb = 1 + (round + N - 1 - k2) % (N - 1);
+        }
+        if (pa > pb) {
+          const int t_ = pa;
+          pa = pb;
+          pb = t_;
+        }
+        const double pc = __shfl_sync(0xffffffffu, c, pa);
+        const double ps = __shfl_sync(0xffffffffu, s, pa);
+        const double pex = __shfl_sync(0xffffffffu, ec, pa);
+        const double pey = __shfl_sync(0xffffffffu, es, pa);
+        if (ps != 0.0) {
+          const cplx epi = cmk(pex, pey);  // e^{i phi}
+          const cplx xp = a[pa], xq = a[pb];
+          const cplx wq = cmul(epi, xq);
+          a[pa] = cmk(pc * xp.x - ps * wq.x, pc * xp.y - ps * wq.y);
+          a[pb] = cmk(ps * xp.x + pc * wq.x, ps * xp.y + pc * wq.y);
+        }
+      }
+      // exact 2x2 block of the own pair
+      if (s != 0.0) {
+        const double nd = is_p ? app - tr : aqq + tr;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          if (k == l) a[k] = cmk(nd, 0.0);
+          if (k == m) a[k] = cmk(0.0, 0.0);
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  if (l < n) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      if (k < n) j.V[k * j.ld + l] = v[k];
+      if (k == l) j.val[l] = a[k].x;
+    }
+  }
+}
+
+__device__ inline void jac_finish(JacSmem& j, int n);
+
+// Block Jacobi + the reference ordering/phase conventions. All threads of the
+// CTA must call. (The register-resident warp_jacobi above measured slower on
+// B200 -- 82 vs 49 us at n = 8, 517 vs 121 us at n = 16 -- because its
+// critical path is the same FP64 rotation chain plus ~60 shuffles per
+// round, so the block version stays the default.)
+__device__ inline void jac_solve(JacSmem& j, const cplx* M, int ldm, int n, double div) {
+  jac_load_sym(j, M, ldm, n, div);
+  jac_sweeps(j, n);
+  jac_finish(j, n);
+}
+
 // Descending order + tie rule + pivot phase. Produces j.order (column of V
 // for output position k) and rotates V's columns in place.
 __device__ inline void jac_finish(JacSmem& j, int n) {

@@ -259,9 +259,7 @@ __device__ int spatial_update(const cplx* V, double nb2, int P, int ra, double t
     }
   } else {
     JacSmem j = jac_carve(sm, P);
-    jac_load_sym(j, V, P, P, nb2);
-    jac_sweeps(j, P);
-    jac_finish(j, P);
+    jac_solve(j, V, P, P, nb2);
     if (tid == 0) {
       double top = 0.0;
       for (int k = 0; k < P; ++k) top = fmax(top, fabs(j.val[k]));

@@ -8,9 +8,7 @@ using namespace kstj;
 __global__ void probe(const cplx* M, int n, int* sweeps, double* vals) {
   extern __shared__ __align__(16) char sm[];
   JacSmem j = jac_carve(sm, n);
-  jac_load_sym(j, M, n, n, 1.0);
-  jac_sweeps(j, n);
-  jac_finish(j, n);
+  jac_solve(j, M, n, n, 1.0);
   if (threadIdx.x == 0) { *sweeps = j.flag[1]; for (int k = 0; k < n; ++k) vals[k] = j.val[j.order[k]]; }
 }
 int main() {

@@ -47,6 +47,49 @@ __global__ void twiddle_kernel(cplx* w, int D) {
   }
 }
 
+// One odd-radix Stockham stage with the butterfly inputs held in registers:
+// each work item j < D/R loads its R inputs once (stage twiddles applied),
+// forms s_r = t_r + t_{R-r}, d_r = t_r - t_{R-r} in place, and emits all R
+// outputs -- shared-memory traffic ~2D per stage instead of ~R*D.
+template <int R>
+__device__ __forceinline__ void stage_reg(const cplx* __restrict__ a, cplx* __restrict__ b,
+                                          const cplx* __restrict__ w, int D, int Ns) {
+  constexpr int h = (R - 1) / 2;
+  const int DR = D / R, step = D / (Ns * R), DRR = D / R;
+  for (int j = threadIdx.x; j < DR; j += blockDim.x) {
+    const int k = j % Ns;
+    cplx t[R];
+    t[0] = a[j];
+#pragma unroll
+    for (int r = 1; r < R; ++r) t[r] = cmul(a[j + r * DR], w[r * k * step]);
+#pragma unroll
+    for (int r = 1; r <= h; ++r) {
+      const cplx sr = cadd(t[r], t[R - r]), dr = csub(t[r], t[R - r]);
+      t[r] = sr;
+      t[R - r] = dr;
+    }
+    const int dst = (j / Ns) * Ns * R + k;
+    cplx x0 = t[0];
+#pragma unroll
+    for (int r = 1; r <= h; ++r) x0 = cadd(x0, t[r]);
+    b[dst] = x0;
+#pragma unroll 1
+    for (int u = 1; u <= h; ++u) {
+      double ax = t[0].x, ay = t[0].y, bx = 0.0, by = 0.0;
+#pragma unroll
+      for (int r = 1; r <= h; ++r) {
+        const cplx wm = w[((r * u) % R) * DRR];  // (cos, -sin) of 2 pi r u / R
+        ax = fma(wm.x, t[r].x, ax);
+        ay = fma(wm.x, t[r].y, ay);
+        bx = fma(-wm.y, t[R - r].x, bx);
+        by = fma(-wm.y, t[R - r].y, by);
+      }
+      b[dst + u * Ns] = cmk(ax + by, ay - bx);        // A - iB
+      b[dst + (R - u) * Ns] = cmk(ax - by, ay + bx);  // A + iB
+    }
+  }
+}
+
 // Ping-pong Stockham DFT (decimation in time) of length D over shared
 // buffers; w[k] = exp(-2 pi i k / D). Stage (radix R, Ns = product of the
 // previous radices, DR = D / R, step = D / (Ns R)), for j < DR, k = j mod Ns:
@@ -86,6 +129,16 @@ __device__ cplx* stockham(cplx* a, cplx* b, const cplx* __restrict__ w, int D) {
           b[dst + 2 * Ns] = csub(s02, s13);
           b[dst + 3 * Ns] = cmk(d02.x - d13.y, d02.y + d13.x);
         }
+      }
+    } else if (R == 3 || R == 5 || R == 7 || R == 11 || R == 13 || R == 23 || R == 29) {
+      switch (R) {
+        case 3: stage_reg<3>(a, b, w, D, Ns); break;
+        case 5: stage_reg<5>(a, b, w, D, Ns); break;
+        case 7: stage_reg<7>(a, b, w, D, Ns); break;
+        case 11: stage_reg<11>(a, b, w, D, Ns); break;
+        case 13: stage_reg<13>(a, b, w, D, Ns); break;
+        case 23: stage_reg<23>(a, b, w, D, Ns); break;
+        default: stage_reg<29>(a, b, w, D, Ns); break;
       }
     } else {
       const int h = (R - 1) / 2;
@@ -145,10 +198,14 @@ __device__ cplx* stockham(cplx* a, cplx* b, const cplx* __restrict__ w, int D) {
 
 // One CTA per row (bin m, channel i) of `src` (rows x q, row stride q):
 // coefficients against U_B and the folded DFT (uniform) or direct sum.
-__global__ void __launch_bounds__(NT) row_spectrum_kernel(
+// 128-thread CTAs: the register-resident radix-23/29 butterflies need ~150
+// registers, so two row-CTAs per SM beat one 256-thread CTA.
+constexpr int NTS = 128;
+__global__ void __launch_bounds__(NTS) row_spectrum_kernel(
     const cplx* __restrict__ src, int64_t rows, int q, const cplx* __restrict__ ub, int kb,
     const cplx* __restrict__ w, int D, int uniform, const double* __restrict__ dop,
     cplx* __restrict__ spec, cplx* __restrict__ coef, int* __restrict__ nonfinite) {
+  constexpr int NT = NTS;  // shadows the file-wide 256
   extern __shared__ __align__(16) cplx smem[];
   __shared__ double red[32];
   const int64_t row = blockIdx.x;
@@ -532,11 +589,11 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
     transpose_kernel<<<cdiv((int64_t)q * kb_used, 256), 256, 0, st>>>(ub, q, kb_used, ubT);
     KST_LAUNCH(ctx);
     // spectra of the temporal basis columns (coefficients unused)
-    row_spectrum_kernel<<<kb_used, NT, smem, st>>>(ubT, kb_used, q, nullptr, 0, tw, D, uniform, dop,
+    row_spectrum_kernel<<<kb_used, NTS, smem, st>>>(ubT, kb_used, q, nullptr, 0, tw, D, uniform, dop,
                                                    ubspec, nullptr, flag + 1);
     KST_LAUNCH(ctx);
   }
-  row_spectrum_kernel<<<(unsigned)rows, NT, smem, st>>>(cube, rows, q, ub, kb_used, tw, D, uniform,
+  row_spectrum_kernel<<<(unsigned)rows, NTS, smem, st>>>(cube, rows, q, ub, kb_used, tw, D, uniform,
                                                         dop, spec, coef, flag);
   KST_LAUNCH(ctx);
   CombineArgs a;

@@ -108,7 +108,7 @@ __global__ void slice_kernel(const cplx* __restrict__ X, int64_t n, int64_t npad
 // CTA per (bi <= bj) pair of 32x32 tiles; writes both S[a][b] and S[b][a].
 // Templated on the slice count so the per-element plane loads are unrolled.
 template <int SS>
-__global__ void __launch_bounds__(256) ozaki_combine_kernel(
+__global__ void __launch_bounds__(256, 4) ozaki_combine_kernel(
     const int32_t* __restrict__ GRe, const int32_t* __restrict__ GM, int64_t dpad, int64_t d,
     const int* __restrict__ expo, double dn, int T, cplx* __restrict__ S) {
   constexpr int s = SS;

@@ -43,16 +43,6 @@ __global__ void gram_prep(const cplx* __restrict__ X, int64_t n, int64_t d, int6
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
 // D(8x8) += A(8x4, row) * B(4x8, col); lane (g = lane/4, t = lane%4) holds
 // a = A[g][t], b = B[t][g], c = {C[g][2t], C[g][2t+1]}.
 __device__ __forceinline__ void dmma(double2& c, double a, double b) {

@@ -66,40 +66,60 @@ __global__ void colmax_kernel(const cplx* __restrict__ X, int64_t n, int64_t d,
 //   If [a][t][k] = sigma_{t+1}(imag),  Rr[a][s-1-t][k] = sigma_{t+1}(real)
 // A prefix of RIf against the matching suffix of RIr pairs (sigma_t, sigma_{e-t})
 // of the same part for every t, so Re = GR_e + GI_e is ONE int8 GEMM per e.
-// 32x32 tiles through smem: X reads coalesced over a, slice writes over k.
-// Padded rows/columns (k >= n, a >= d) are written as zero slices.
-__global__ void slice_kernel(const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d,
-                             int64_t dpad, const int* __restrict__ expo, int s,
-                             int8_t* __restrict__ RIf, int8_t* __restrict__ RIr,
-                             int8_t* __restrict__ If, int8_t* __restrict__ Rr) {
-  __shared__ cplx tile[32][33];
-  const int64_t k0 = (int64_t)blockIdx.y * 32, a0 = (int64_t)blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t k = k0 + r, a = a0 + tx;
-    tile[r][tx] = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+// CTA = 16 columns a x 128 rows k. Phase 1 reads X coalesced over a and cuts
+// each element into its 2s slice bytes, staged in smem as [part][t][a][k];
+// phase 2 writes every (a, slice) row segment with 4-byte stores coalesced
+// over k (128 contiguous bytes per warp store). Padded rows/columns
+// (k >= n, a >= d) are written as zero slices.
+constexpr int SL_A = 16, SL_K = 128, SL_KP = SL_K + 4;
+template <int SS>
+__global__ void __launch_bounds__(256) slice_kernel(
+    const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d, int64_t dpad,
+    const int* __restrict__ expo, int8_t* __restrict__ RIf, int8_t* __restrict__ RIr,
+    int8_t* __restrict__ If, int8_t* __restrict__ Rr) {
+  constexpr int s = SS;
+  __shared__ __align__(16) int8_t sb[2][s][SL_A][SL_KP];
+  const int64_t k0 = (int64_t)blockIdx.y * SL_K, a0 = (int64_t)blockIdx.x * SL_A;
+  const int tid = threadIdx.x;
+  {
+    const int c = tid & (SL_A - 1);
+    const int64_t a = a0 + c;
+    const int e = a < d ? expo[a] : 0;
+    const double sc = (e == kNaNExpo) ? 0.0 : ldexp(1.0, -e);
+    for (int r = tid / SL_A; r < SL_K; r += 256 / SL_A) {
+      const int64_t k = k0 + r;
+      const cplx v = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+      double rr = v.x * sc, ri = v.y * sc;  // |.| < 1
+#pragma unroll
+      for (int t = 0; t < s; ++t) {
+        rr *= 128.0;
+        ri *= 128.0;
+        const double qr = trunc(rr), qi = trunc(ri);
+        rr -= qr;  // exact
+        ri -= qi;
+        sb[0][t][c][r] = (int8_t)qr;
+        sb[1][t][c][r] = (int8_t)qi;
+      }
+    }
   }
   __syncthreads();
-  for (int c = ty; c < 32; c += 8) {
-    const int64_t a = a0 + c, k = k0 + tx;
-    if (a >= dpad || k >= npad) continue;
-    const int e = a < d ? expo[a] : 0;
-    const cplx v = tile[tx][c];
-    const double sc = (e == kNaNExpo) ? 0.0 : ldexp(1.0, -e);
-    double rr = v.x * sc, ri = v.y * sc;  // |.| < 1
+  const int lane = tid & 31, w = tid >> 5;
+  const int64_t k = k0 + 4 * lane;
+  if (k >= npad) return;  // npad is a multiple of 16: whole words only
+  for (int c = w; c < SL_A; c += 8) {
+    const int64_t a = a0 + c;
+    if (a >= dpad) break;
     const int64_t b2 = a * (int64_t)(2 * s) * npad + k, b1 = a * (int64_t)s * npad + k;
+#pragma unroll
     for (int t = 0; t < s; ++t) {
-      rr *= 128.0;
-      ri *= 128.0;
-      const double qr = trunc(rr), qi = trunc(ri);
-      rr -= qr;  // exact
-      ri -= qi;
-      RIf[b2 + (int64_t)(2 * t) * npad] = (int8_t)qr;
-      RIf[b2 + (int64_t)(2 * t + 1) * npad] = (int8_t)qi;
-      RIr[b2 + (int64_t)(2 * (s - 1 - t)) * npad] = (int8_t)qr;
-      RIr[b2 + (int64_t)(2 * (s - 1 - t) + 1) * npad] = (int8_t)qi;
-      If[b1 + (int64_t)t * npad] = (int8_t)qi;
-      Rr[b1 + (int64_t)(s - 1 - t) * npad] = (int8_t)qr;
+      const uint32_t qr = *(const uint32_t*)&sb[0][t][c][4 * lane];
+      const uint32_t qi = *(const uint32_t*)&sb[1][t][c][4 * lane];
+      *(uint32_t*)(RIf + b2 + (int64_t)(2 * t) * npad) = qr;
+      *(uint32_t*)(RIf + b2 + (int64_t)(2 * t + 1) * npad) = qi;
+      *(uint32_t*)(RIr + b2 + (int64_t)(2 * (s - 1 - t)) * npad) = qr;
+      *(uint32_t*)(RIr + b2 + (int64_t)(2 * (s - 1 - t) + 1) * npad) = qi;
+      *(uint32_t*)(If + b1 + (int64_t)t * npad) = qi;
+      *(uint32_t*)(Rr + b1 + (int64_t)(s - 1 - t) * npad) = qr;
     }
   }
 }
@@ -108,7 +128,7 @@ __global__ void slice_kernel(const cplx* __restrict__ X, int64_t n, int64_t npad
 // CTA per (bi <= bj) pair of 32x32 tiles; writes both S[a][b] and S[b][a].
 // Templated on the slice count so the per-element plane loads are unrolled.
 template <int SS>
-__global__ void __launch_bounds__(256, 4) ozaki_combine_kernel(
+__global__ void __launch_bounds__(256, 2) ozaki_combine_kernel(
     const int32_t* __restrict__ GRe, const int32_t* __restrict__ GM, int64_t dpad, int64_t d,
     const int* __restrict__ expo, double dn, int T, cplx* __restrict__ S) {
   constexpr int s = SS;
@@ -123,55 +143,67 @@ __global__ void __launch_bounds__(256, 4) ozaki_combine_kernel(
   while ((bi + 1) * T - (bi + 1) * bi / 2 <= t) ++bi;
   const int bj = bi + (t - (bi * T - bi * (bi - 1) / 2));
   const int64_t a0 = (int64_t)bi * 32, b0 = (int64_t)bj * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  const int q4 = 4 * (tid & 7), r = tid >> 3;  // 4 consecutive column-major entries per thread
   const size_t plane = (size_t)dpad * dpad;
-  // transposed M block: element (row b0+i, col a0+j) -> column-major index (b0+i) + (a0+j)*dpad
   // exact weights 2^-7e, accumulated from the smallest term (e = s+1) up.
-  // All s loads of an element are issued before any is consumed (unrolled,
-  // predicated), so the kernel streams instead of serialising on latency.
+  // Each thread issues all its 16-byte plane loads before consuming any.
   const double w0 = ldexp(1.0, -7 * (s + 1));
-  for (int i = ty; i < 32; i += 8) {
-    const size_t idx = (size_t)(b0 + tx) + (size_t)(a0 + i) * dpad;  // M[b0+tx][a0+i]
-    int32_t v[8];
+  {  // transposed M block: mt[i][j] = M[b0+i][a0+j], column-major index (b0+i) + (a0+j)*dpad
+    const size_t idx = (size_t)(b0 + q4) + (size_t)(a0 + r) * dpad;
+    int4 v[s];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = (u < s) ? GM[(size_t)(s - 1 - u) * plane + idx] : 0;
-    double acc = 0.0, w = w0;
+    for (int u = 0; u < s; ++u) v[u] = *(const int4*)(GM + (size_t)(s - 1 - u) * plane + idx);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0}, w = w0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u < s) {
-        acc += (double)v[u] * w;
-        w *= 128.0;
-      }
-    mt[tx][i] = acc;  // mt[b-offset][a-offset]
+    for (int u = 0; u < s; ++u) {
+      acc[0] += (double)v[u].x * w;
+      acc[1] += (double)v[u].y * w;
+      acc[2] += (double)v[u].z * w;
+      acc[3] += (double)v[u].w * w;
+      w *= 128.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) mt[q4 + c][r] = acc[c];
   }
   __syncthreads();
-  // (a = a0 + tx, b = b0 + i): column-major G reads coalesced over tx
-  for (int i = ty; i < 32; i += 8) {
-    const int64_t a = a0 + tx, b = b0 + i;
-    const size_t idx = (size_t)a + (size_t)b * dpad;  // G[a][b]
-    int32_t vr[8], vm[8];
+  {  // (a = a0 + q4 + c, b = b0 + r): column-major G[a][b] at a + b*dpad
+    const int64_t b = b0 + r;
+    const size_t idx = (size_t)(a0 + q4) + (size_t)b * dpad;
+    int4 vr[s], vm[s];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      vr[u] = (u < s) ? GRe[(size_t)(s - 1 - u) * plane + idx] : 0;
-      vm[u] = (u < s) ? GM[(size_t)(s - 1 - u) * plane + idx] : 0;
+    for (int u = 0; u < s; ++u) {
+      vr[u] = *(const int4*)(GRe + (size_t)(s - 1 - u) * plane + idx);
+      vm[u] = *(const int4*)(GM + (size_t)(s - 1 - u) * plane + idx);
     }
-    double re = 0.0, m_ab = 0.0, w = w0;
+    double re[4] = {0.0, 0.0, 0.0, 0.0}, m_ab[4] = {0.0, 0.0, 0.0, 0.0}, w = w0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u < s) {
-        re += (double)vr[u] * w;
-        m_ab += (double)vm[u] * w;
-        w *= 128.0;
+    for (int u = 0; u < s; ++u) {
+      re[0] += (double)vr[u].x * w;
+      re[1] += (double)vr[u].y * w;
+      re[2] += (double)vr[u].z * w;
+      re[3] += (double)vr[u].w * w;
+      m_ab[0] += (double)vm[u].x * w;
+      m_ab[1] += (double)vm[u].y * w;
+      m_ab[2] += (double)vm[u].z * w;
+      m_ab[3] += (double)vm[u].w * w;
+      w *= 128.0;
+    }
+    const int eb = (b < d) ? expo[b] : 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t a = a0 + q4 + c;
+      const double im = m_ab[c] - mt[r][q4 + c];  // M[a][b] - M[b][a]
+      const int ea = (a < d) ? expo[a] : 0;
+      cplx v;
+      if (ea == kNaNExpo || eb == kNaNExpo) {
+        v = cmk(NAN, NAN);
+      } else {
+        v = cmk(ldexp(re[c], ea + eb) / dn, ldexp(im, ea + eb) / dn);
       }
-    const double im = m_ab - mt[i][tx];  // M[a][b] - M[b][a]
-    const int ea = (a < d) ? expo[a] : 0, eb = (b < d) ? expo[b] : 0;
-    cplx v;
-    if (ea == kNaNExpo || eb == kNaNExpo) {
-      v = cmk(NAN, NAN);
-    } else {
-      v = cmk(ldexp(re, ea + eb) / dn, ldexp(im, ea + eb) / dn);
+      vt[q4 + c][r] = v;
     }
-    vt[tx][i] = v;
   }
   __syncthreads();
   // row-major S writes, coalesced over the column index
@@ -289,9 +321,21 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
 
   colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
   KST_LAUNCH(ctx);
-  slice_kernel<<<dim3(cdiv(dpad, 32), cdiv(npad, 32)), dim3(32, 8), 0, st>>>(
-      X, n, npad, d, dpad, expo, s, RIf, RIr, If, Rr);
-  KST_LAUNCH(ctx);
+  {
+    const dim3 grid(cdiv(dpad, SL_A), cdiv(npad, SL_K));
+#define KST_SLICE(S_)                                                                            \
+  slice_kernel<S_><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, RIf, RIr, If, Rr)
+    switch (s) {
+      case 3: KST_SLICE(3); break;
+      case 4: KST_SLICE(4); break;
+      case 5: KST_SLICE(5); break;
+      case 6: KST_SLICE(6); break;
+      case 7: KST_SLICE(7); break;
+      default: KST_SLICE(8); break;
+    }
+#undef KST_SLICE
+    KST_LAUNCH(ctx);
+  }
   stage_mark(ctx, 5, st);  // profiling: int8 GEMM span (events 5..6)
   const int32_t one = 1, zero = 0;
   const int lda2 = (int)(2 * s * npad), lda1 = (int)(s * npad);
@@ -333,7 +377,7 @@ int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s,
   }
   const int T = (int)(dpad / 32);
   const unsigned nt = T * (T + 1) / 2;
-  const dim3 blk(32, 8);
+  const unsigned blk = 256;
   switch (s) {
     case 3: ozaki_combine_kernel<3><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;
     case 4: ozaki_combine_kernel<4><<<nt, blk, 0, st>>>(GRe, GM, dpad, d, expo, (double)n, T, S); break;

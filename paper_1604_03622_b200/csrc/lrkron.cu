@@ -570,6 +570,157 @@ __global__ void __launch_bounds__(NT, 1) mgram_reg_kernel(const cplx* __restrict
   (void)E;
 }
 
+// Split register variant (P = 3: 45 complex M entries do not fit one thread's
+// registers). The CTA is NG groups of 128 threads over `rows` rows of S4.
+// Tiles of 128 positions x U blocks stream through an MS_STAGES-deep cp.async
+// ring in smem (loads decoupled from registers, so the SM keeps ~55 KB in
+// flight); every group reads each position's s-vector from the ring and
+// group g owns a contiguous chunk [ms_bound(g), ms_bound(g+1)) of the upper
+// triangle; group 0 also owns the scans and block sums. Same partial record
+// as mgram_kernel.
+constexpr int MS_NTG = 128;  // threads per group = positions per tile
+constexpr int MS_STAGES = 4;
+// chunk bounds: group 0 (which also carries the scans) takes a smaller share
+__host__ __device__ constexpr int ms_bound(int E, int NG, int g) {
+  return g <= 0 ? 0
+         : g >= NG ? E
+         : (E / NG - (E / NG / 2 < 6 ? E / NG / 2 : 6)) +
+               (E - (E / NG - (E / NG / 2 < 6 ? E / NG / 2 : 6))) * (g - 1) / (NG - 1);
+}
+template <int P, int NG, int G>
+__device__ __forceinline__ void mgram_split_group(const cplx* __restrict__ S, int q, int r0,
+                                                  int rows, int tg, cplx* __restrict__ ring,
+                                                  double (*red)[MDims<P>::STRIDE]) {
+  using Dm = MDims<P>;
+  constexpr int U = Dm::U, E = Dm::E;
+  constexpr int K0 = ms_bound(E, NG, G), K1 = ms_bound(E, NG, G + 1), NK = K1 - K0;
+  constexpr int NS = (G == 0) ? 4 + 2 * U : 0;  // scan + block-sum slots
+  const int64_t d = (int64_t)P * q;
+  double st[NS > 0 ? NS : 1], m[2 * NK];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) st[k] = 0.0;
+  if (NS) {
+    st[2] = 1e308;
+    st[3] = -1e308;
+  }
+#pragma unroll
+  for (int k = 0; k < 2 * NK; ++k) m[k] = 0.0;
+  const int nct = (q + MS_NTG - 1) / MS_NTG;
+  const int ntile = rows * nct;
+  // every thread of the CTA issues its share of a tile; empty groups keep counts aligned
+  auto issue = [&](int t) {
+    if (t < ntile) {
+      const int r = r0 + t / nct, c0 = (t % nct) * MS_NTG;
+      cplx* buf = ring + (size_t)(t % MS_STAGES) * U * MS_NTG;
+      for (int e = threadIdx.x; e < U * MS_NTG; e += NG * MS_NTG) {
+        const int u = e / MS_NTG, pp = e % MS_NTG, c = c0 + pp;
+        if (c < q)
+          cp_async16(buf + e, S + ((int64_t)(u / P) * q + r) * d + (int64_t)(u % P) * q + c);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll 1
+  for (int t = 0; t < MS_STAGES - 1; ++t) issue(t);
+#pragma unroll 1
+  for (int t = 0; t < ntile; ++t) {
+    cp_async_wait<MS_STAGES - 2>();
+    __syncthreads();  // tile t visible to all; buffer of tile t-1 free
+    issue(t + MS_STAGES - 1);
+    const int r = r0 + t / nct, c = (t % nct) * MS_NTG + tg;
+    if (c < q) {
+      const cplx* buf = ring + (size_t)(t % MS_STAGES) * U * MS_NTG + tg;
+      cplx sv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) sv[u] = buf[u * MS_NTG];
+      if (NS) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const cplx v = sv[u];
+          if (!isfinite(v.x) || !isfinite(v.y)) st[1] += 1.0;
+          st[0] = fma(v.x, v.x, st[0]);
+          st[0] = fma(v.y, v.y, st[0]);
+          st[4 + 2 * u] += v.x;
+          st[4 + 2 * u + 1] += v.y;
+          if (u / P == u % P && c == r) {
+            st[2] = fmin(st[2], v.x);
+            st[3] = fmax(st[3], v.x);
+          }
+        }
+      }
+      int k = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int v = u; v < U; ++v, ++k)
+          if (k >= K0 && k < K1) {
+            const cplx a = sv[u], b = sv[v];  // M_uv += s_u conj(s_v)
+            double& mr = m[2 * (k - K0)];
+            double& mi = m[2 * (k - K0) + 1];
+            mr = fma(a.x, b.x, mr);
+            mr = fma(a.y, b.y, mr);
+            mi = fma(a.y, b.x, mi);
+            mi = fma(-a.x, b.y, mi);
+          }
+    }
+  }
+  cp_async_wait<0>();
+  const int w = tg >> 5, l = tg & 31, wrow = G * (MS_NTG / 32) + w;
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    double v = st[k];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, v, o);
+      v = (k == 2) ? fmin(v, x) : (k == 3) ? fmax(v, x) : v + x;
+    }
+    if (l == 0) red[wrow][k] = v;
+  }
+#pragma unroll
+  for (int k = 0; k < 2 * NK; ++k) {
+    double v = m[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (l == 0) red[wrow][4 + 2 * U + 2 * K0 + k] = v;
+  }
+}
+
+template <int P, int NG>
+__global__ void __launch_bounds__(NG * MS_NTG, 1) mgram_split_kernel(const cplx* __restrict__ S,
+                                                                     int q, int rows_per,
+                                                                     double* __restrict__ part) {
+  static_assert(NG >= 1 && NG <= 4, "mgram_split_kernel: 1..4 groups");
+  using Dm = MDims<P>;
+  constexpr int U = Dm::U, E = Dm::E, R = Dm::STRIDE, WG = MS_NTG / 32;
+  __shared__ double red[NG * WG][R];
+  extern __shared__ __align__(16) unsigned char ms_dyn[];
+  cplx* ring = (cplx*)ms_dyn;  // MS_STAGES x U x MS_NTG
+  const int g = threadIdx.x / MS_NTG, tg = threadIdx.x % MS_NTG;
+  const int r0 = blockIdx.x * rows_per;
+  const int rows = min(rows_per, q - r0);
+  // the groups run different instantiations; their barriers are CTA-wide bar.sync 0
+  // reached the same number of times by every warp
+  if (g == 0) mgram_split_group<P, NG, 0>(S, q, r0, rows, tg, ring, red);
+  if (NG > 1 && g == 1) mgram_split_group<P, NG, (NG > 1 ? 1 : 0)>(S, q, r0, rows, tg, ring, red);
+  if (NG > 2 && g == 2) mgram_split_group<P, NG, (NG > 2 ? 2 : 0)>(S, q, r0, rows, tg, ring, red);
+  if (NG > 3 && g == 3) mgram_split_group<P, NG, (NG > 3 ? 3 : 0)>(S, q, r0, rows, tg, ring, red);
+  __syncthreads();
+  double* out = part + (size_t)blockIdx.x * R;
+  for (int k = threadIdx.x; k < R; k += NG * MS_NTG) {
+    // owner group: the largest g with ms_bound(g) <= entry (scans belong to group 0)
+    int owner = 0;
+    if (k >= 4 + 2 * U) {
+      const int ent = (k - 4 - 2 * U) >> 1;
+      for (int gg = 1; gg < NG; ++gg)
+        if (ms_bound(E, NG, gg) <= ent) owner = gg;
+    }
+    double v = red[owner * WG][k];
+    for (int ww = 1; ww < WG; ++ww) {
+      const double x = red[owner * WG + ww][k];
+      v = (k == 2) ? fmin(v, x) : (k == 3) ? fmax(v, x) : v + x;
+    }
+    out[k] = v;
+  }
+}
+
 // Reduce mgram partials (fixed order) and run ALL iterations in one CTA.
 // Outputs: spatial (final A), residuals[max_iter], info[0..3] = {status,
 // iterations, converged, pad}, host_diag[0..4] = {bad, dmin, dmax, fro, na2_0};
@@ -757,7 +908,16 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   double* mres = nullptr;
   double* minfo = nullptr;
   if (mpath) {
-    const int nblk = (q + MG_ROWS - 1) / MG_ROWS;
+    // P = 3: one wave of pipelined CTAs (rows_per rows each); others MG_ROWS rows
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      if (nsm <= 0) nsm = 148;
+    }
+    const int rows_per = p == 3 ? (q + nsm - 1) / nsm : MG_ROWS;
+    const int nblk = (q + rows_per - 1) / rows_per;
     size_t rec = 0;
     KST_DISPATCH_P(p, (rec = MDims<PP>::STRIDE));
     double* mpart = (double*)ws_get(ctx, WS_PART, sizeof(double) * rec * nblk + 64);
@@ -778,7 +938,12 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
                                                  dres, minfo, (double*)(small + sizeof(IterState)));
         break;
       case 3:
-        mgram_reg_kernel<3><<<nblk, NT, 0, st>>>(S, q, mpart);
+      {
+        constexpr size_t ring = sizeof(cplx) * MS_STAGES * 9 * MS_NTG;
+        KST_CUDA(ctx, cudaFuncSetAttribute(mgram_split_kernel<3, 3>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring));
+        mgram_split_kernel<3, 3><<<nblk, 3 * MS_NTG, ring, st>>>(S, q, rows_per, mpart);
+      }
         m_iterate_kernel<3><<<1, NT, jsm, st>>>(mpart, nblk, q, ra, tol, max_iter, state, spatial,
                                                  dres, minfo, (double*)(small + sizeof(IterState)));
         break;

@@ -30,10 +30,19 @@ constexpr int kMaxFactors = 32;
 constexpr int kMaxP = 16;
 constexpr int kMaxKB = 64;
 
+// Odd radices with register-resident butterflies; their W_R^m = (cos, -sin)
+// of 2 pi m / R live in the plan (constant bank) at offset rtw_off(R).
+constexpr int kRegRadix[] = {3, 5, 7, 11, 13, 23, 29};
+__host__ __device__ constexpr int rtw_off(int R) {
+  return R == 3 ? 0 : R == 5 ? 3 : R == 7 ? 8 : R == 11 ? 15 : R == 13 ? 26 : R == 23 ? 39 : 62;
+}
+constexpr int kRtwCount = 91;  // sum of kRegRadix
+
 struct Plan {
   int D;
   int nf;
   int radix[kMaxFactors];
+  double rtw[2 * kRtwCount];
 };
 
 __constant__ Plan c_plan;
@@ -55,7 +64,8 @@ template <int R>
 __device__ __forceinline__ void stage_reg(const cplx* __restrict__ a, cplx* __restrict__ b,
                                           const cplx* __restrict__ w, int D, int Ns) {
   constexpr int h = (R - 1) / 2;
-  const int DR = D / R, step = D / (Ns * R), DRR = D / R;
+  constexpr int off = rtw_off(R);
+  const int DR = D / R, step = D / (Ns * R);
   for (int j = threadIdx.x; j < DR; j += blockDim.x) {
     const int k = j % Ns;
     cplx t[R];
@@ -73,16 +83,19 @@ __device__ __forceinline__ void stage_reg(const cplx* __restrict__ a, cplx* __re
 #pragma unroll
     for (int r = 1; r <= h; ++r) x0 = cadd(x0, t[r]);
     b[dst] = x0;
-#pragma unroll 1
+    // fully unrolled: (r u) mod R is a compile-time constant, so every
+    // W_R^m operand is a constant-bank read folded into the DFMA
+#pragma unroll
     for (int u = 1; u <= h; ++u) {
       double ax = t[0].x, ay = t[0].y, bx = 0.0, by = 0.0;
 #pragma unroll
       for (int r = 1; r <= h; ++r) {
-        const cplx wm = w[((r * u) % R) * DRR];  // (cos, -sin) of 2 pi r u / R
-        ax = fma(wm.x, t[r].x, ax);
-        ay = fma(wm.x, t[r].y, ay);
-        bx = fma(-wm.y, t[R - r].x, bx);
-        by = fma(-wm.y, t[R - r].y, by);
+        const int m = (r * u) % R;
+        const double wc = c_plan.rtw[2 * (off + m)], ws = c_plan.rtw[2 * (off + m) + 1];
+        ax = fma(wc, t[r].x, ax);
+        ay = fma(wc, t[r].y, ay);
+        bx = fma(-ws, t[R - r].x, bx);
+        by = fma(-ws, t[R - r].y, by);
       }
       b[dst + u * Ns] = cmk(ax + by, ay - bx);        // A - iB
       b[dst + (R - u) * Ns] = cmk(ax - by, ay + bx);  // A + iB
@@ -210,6 +223,32 @@ __global__ void __launch_bounds__(NTS) row_spectrum_kernel(
   __shared__ double red[32];
   const int64_t row = blockIdx.x;
   const cplx* x = src + row * q;
+  // 0. stage the row (and the twiddle table) in smem with one batch of
+  //    cp.async copies: every load is in flight at once instead of one
+  //    dependent global load per loop trip.
+  //    Uniform grid with q <= D: the row lands in the FFT input buffer
+  //    (zero-padded to D); otherwise in the first q entries of smem.
+  const bool staged_fft = uniform && q <= D;
+  cplx* xs = smem;  // staged row (both paths start at smem[0])
+  if (uniform) {
+    cplx* tw = smem + 2 * D;
+    for (int k = threadIdx.x; k < D; k += NT) {
+      cp_async16(&tw[k], &w[k]);
+      if (staged_fft) {
+        if (k < q)
+          cp_async16(&xs[k], &x[k]);
+        else
+          xs[k] = cmk(0, 0);
+      }
+    }
+  } else {
+    for (int t = threadIdx.x; t < q; t += NT) cp_async16(&xs[t], &x[t]);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const bool in_smem = staged_fft || !uniform;
+  const cplx* xr = in_smem ? xs : x;
   // 1. temporal coefficients c[k] = sum_t x[t] conj(ub[t, k]), 4 at a time,
   //    one fixed-order multi-value block reduction per group
   int bad = 0;
@@ -218,8 +257,9 @@ __global__ void __launch_bounds__(NTS) row_spectrum_kernel(
     double acc[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 4
     for (int t = threadIdx.x; t < q; t += NT) {
-      const cplx v = x[t];
+      const cplx v = xr[t];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (k0 + u < kb) {
@@ -254,29 +294,32 @@ __global__ void __launch_bounds__(NTS) row_spectrum_kernel(
     cplx* a = smem;
     cplx* b = smem + D;
     cplx* tw = smem + 2 * D;
-    for (int k = threadIdx.x; k < D; k += NT) tw[k] = w[k];
-    // 2. fold t mod D (ascending t: deterministic)
-    for (int tp = threadIdx.x; tp < D; tp += NT) {
-      cplx acc = cmk(0, 0);
-      for (int t = tp; t < q; t += D) {
-        const cplx v = x[t];
+    if (staged_fft) {
+      for (int t = threadIdx.x; t < q; t += NT) {
+        const cplx v = a[t];
         if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
-        acc = cadd(acc, v);
       }
-      a[tp] = acc;
+    } else {
+      // 2. fold t mod D (ascending t: deterministic)
+      for (int tp = threadIdx.x; tp < D; tp += NT) {
+        cplx acc = cmk(0, 0);
+        for (int t = tp; t < q; t += D) {
+          const cplx v = x[t];
+          if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+          acc = cadd(acc, v);
+        }
+        a[tp] = acc;
+      }
     }
     __syncthreads();
     cplx* res = stockham(a, b, tw, D);
     for (int d = threadIdx.x; d < D; d += NT) spec[row * D + d] = res[d];
   } else {
     // direct sum with the reference's phase: theta = 2 pi (t f_d)
-    cplx* xs = smem;
     for (int t = threadIdx.x; t < q; t += NT) {
-      const cplx v = x[t];
+      const cplx v = xs[t];
       if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
-      xs[t] = v;
     }
-    __syncthreads();
     const double twopi = 6.283185307179586;
     for (int d = threadIdx.x; d < D; d += NT) {
       const double f = dop[d];
@@ -309,8 +352,11 @@ struct CombineArgs {
   double inv_sqrt_q;
 };
 
-// grid: (ceil(D / NT), n). One thread per Doppler. Templated on the channel
-// count so the per-pixel channel loops are fully unrolled in registers.
+// grid: (ceil(D / NT), ceil(n / CB_BINS)). One thread per Doppler; each CTA
+// walks CB_BINS consecutive bins so the per-CTA setup (projector, candidate
+// grid in smem) is amortised. Templated on the channel count so the
+// per-pixel channel loops are fully unrolled in registers.
+constexpr int CB_BINS = 8;
 template <int PT>
 __global__ void __launch_bounds__(NT) combine_kernel(
     const cplx* __restrict__ spec, const cplx* __restrict__ coef, const cplx* __restrict__ ubspec,
@@ -318,77 +364,80 @@ __global__ void __launch_bounds__(NT) combine_kernel(
     double* __restrict__ values, int64_t n) {
   __shared__ cplx s_ua[kMaxP * kMaxP];
   __shared__ cplx s_c[kMaxP * kMaxKB];
+  __shared__ cplx s_e[kMaxP * kMaxKB];
   extern __shared__ __align__(16) cplx s_h[];  // G x P conj grid
-  const int64_t m = blockIdx.y;
   constexpr int P = PT;
   for (int e = threadIdx.x; e < P * a.ka; e += NT) s_ua[e] = ua[e];
   for (int e = threadIdx.x; e < a.G * P; e += NT) s_h[e] = hconj[e];
-  if (a.mode != 2) {
-    for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = coef[m * P * a.kb + e];
-  }
-  __syncthreads();
-  if (a.mode == 1) {
-    // classical: E = U_A (U_A^H c)  (src/filters.py:115-116)
-    __shared__ cplx s_e[kMaxP * kMaxKB];
-    for (int e = threadIdx.x; e < P * a.kb; e += NT) {
-      const int i = e / a.kb, k = e % a.kb;
-      cplx acc = cmk(0, 0);
-      for (int al = 0; al < a.ka; ++al) {
-        cplx inner = cmk(0, 0);
-        for (int j = 0; j < P; ++j) cfmca(inner, s_ua[j * a.ka + al], s_c[j * a.kb + k]);
-        cfma(acc, s_ua[i * a.ka + al], inner);
-      }
-      s_e[e] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = s_e[e];
-    __syncthreads();
-  }
   const int d = blockIdx.x * NT + threadIdx.x;
-  if (d >= a.D) return;
-  cplx y[kMaxP];
-#pragma unroll
-  for (int i = 0; i < kMaxP; ++i)
-    if (i < P) y[i] = spec[(m * P + i) * a.D + d];
-  if (a.mode != 2) {
-    for (int k = 0; k < a.kb; ++k) {
-      const cplx u = ubspec[(int64_t)k * a.D + d];
-#pragma unroll
-      for (int i = 0; i < kMaxP; ++i)
-        if (i < P) {
-          const cplx cu = cmul(s_c[i * a.kb + k], u);
-          y[i] = csub(y[i], cu);
-        }
-    }
-  }
-  if (a.spatial) {
-    for (int al = 0; al < a.ka; ++al) {
-      cplx alpha = cmk(0, 0);
-#pragma unroll
-      for (int i = 0; i < kMaxP; ++i)
-        if (i < P) cfmca(alpha, s_ua[i * a.ka + al], y[i]);
-#pragma unroll
-      for (int i = 0; i < kMaxP; ++i)
-        if (i < P) y[i] = csub(y[i], cmul(s_ua[i * a.ka + al], alpha));
-    }
-  }
   const int per = a.G / a.groups;
-  for (int gr = 0; gr < a.groups; ++gr) {
-    // max_g |z_g|: select by |z|^2, then one hypot (|.| as numpy computes it)
-    double best2 = -1.0;
-    cplx zb = cmk(0, 0);
-    for (int g = gr * per; g < (gr + 1) * per; ++g) {
-      cplx z = cmk(0, 0);
+  const int64_t m_end = min((int64_t)(blockIdx.y + 1) * CB_BINS, n);
+  for (int64_t m = (int64_t)blockIdx.y * CB_BINS; m < m_end; ++m) {
+    __syncthreads();  // previous bin's s_c fully consumed
+    if (a.mode != 2) {
+      for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = coef[m * P * a.kb + e];
+    }
+    __syncthreads();
+    if (a.mode == 1) {
+      // classical: E = U_A (U_A^H c)  (src/filters.py:115-116)
+      for (int e = threadIdx.x; e < P * a.kb; e += NT) {
+        const int i = e / a.kb, k = e % a.kb;
+        cplx acc = cmk(0, 0);
+        for (int al = 0; al < a.ka; ++al) {
+          cplx inner = cmk(0, 0);
+          for (int j = 0; j < P; ++j) cfmca(inner, s_ua[j * a.ka + al], s_c[j * a.kb + k]);
+          cfma(acc, s_ua[i * a.ka + al], inner);
+        }
+        s_e[e] = acc;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = s_e[e];
+      __syncthreads();
+    }
+    if (d >= a.D) continue;
+    cplx y[kMaxP];
 #pragma unroll
-      for (int i = 0; i < kMaxP; ++i)
-        if (i < P) cfma(z, s_h[g * P + i], y[i]);
-      const double m2 = cabs2(z);
-      if (m2 > best2) {
-        best2 = m2;
-        zb = z;
+    for (int i = 0; i < kMaxP; ++i)
+      if (i < P) y[i] = spec[(m * P + i) * a.D + d];
+    if (a.mode != 2) {
+      for (int k = 0; k < a.kb; ++k) {
+        const cplx u = ubspec[(int64_t)k * a.D + d];
+#pragma unroll
+        for (int i = 0; i < kMaxP; ++i)
+          if (i < P) {
+            const cplx cu = cmul(s_c[i * a.kb + k], u);
+            y[i] = csub(y[i], cu);
+          }
       }
     }
-    values[((int64_t)gr * n + m) * a.D + d] = hypot(zb.x * a.inv_sqrt_q, zb.y * a.inv_sqrt_q);
+    if (a.spatial) {
+      for (int al = 0; al < a.ka; ++al) {
+        cplx alpha = cmk(0, 0);
+#pragma unroll
+        for (int i = 0; i < kMaxP; ++i)
+          if (i < P) cfmca(alpha, s_ua[i * a.ka + al], y[i]);
+#pragma unroll
+        for (int i = 0; i < kMaxP; ++i)
+          if (i < P) y[i] = csub(y[i], cmul(s_ua[i * a.ka + al], alpha));
+      }
+    }
+    for (int gr = 0; gr < a.groups; ++gr) {
+      // max_g |z_g|: select by |z|^2, then one hypot (|.| as numpy computes it)
+      double best2 = -1.0;
+      cplx zb = cmk(0, 0);
+      for (int g = gr * per; g < (gr + 1) * per; ++g) {
+        cplx z = cmk(0, 0);
+#pragma unroll
+        for (int i = 0; i < kMaxP; ++i)
+          if (i < P) cfma(z, s_h[g * P + i], y[i]);
+        const double m2 = cabs2(z);
+        if (m2 > best2) {
+          best2 = m2;
+          zb = z;
+        }
+      }
+      values[((int64_t)gr * n + m) * a.D + d] = hypot(zb.x * a.inv_sqrt_q, zb.y * a.inv_sqrt_q);
+    }
   }
 }
 
@@ -520,6 +569,12 @@ int plan_factors(int D, Plan& p) {
       x /= f;
     }
   if (x > 1) p.radix[p.nf++] = x;
+  for (int R : kRegRadix)
+    for (int m = 0; m < R; ++m) {
+      const long double th = 2.0L * 3.141592653589793238462643383279502884L * m / R;
+      p.rtw[2 * (rtw_off(R) + m)] = (double)cosl(th);
+      p.rtw[2 * (rtw_off(R) + m) + 1] = (double)-sinl(th);
+    }
   return p.nf <= kMaxFactors;
 }
 
@@ -606,7 +661,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   a.mode = mode;
   a.spatial = spatial;
   a.inv_sqrt_q = 1.0 / sqrt((double)q);
-  KST_DISPATCH_P(p, (combine_kernel<PP><<<dim3(cdiv(D, NT), (unsigned)n), NT,
+  KST_DISPATCH_P(p, (combine_kernel<PP><<<dim3(cdiv(D, NT), cdiv(n, CB_BINS)), NT,
                                           sizeof(cplx) * G * p, st>>>(
                         spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n)));
   KST_LAUNCH(ctx);

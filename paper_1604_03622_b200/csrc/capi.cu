@@ -97,8 +97,17 @@ int kst_ctx_create(int device, kst_ctx** out) {
   // Override: KST_GRAM=int8|dmma, KST_GRAM_SLICES=3..8.
   c->gram_slices = 6;
   c->gram_mode = kst::ozaki_available() ? 1 : 0;
-  if (const char* e = getenv("KST_GRAM")) c->gram_mode = (strcmp(e, "int8") == 0 && kst::ozaki_available()) ? 1 : 0;
-  if (const char* e = getenv("KST_GRAM_SLICES")) c->gram_slices = std::min(8, std::max(3, atoi(e)));
+  if (const char* e = getenv("KST_GRAM")) {
+    const bool i8 = kst::ozaki_available();
+    c->gram_mode = (strcmp(e, "int8") == 0 && i8)                               ? 1
+                   : (strcmp(e, "crt") == 0 && kst::crt_tc_available())        ? 2
+                   : (strcmp(e, "crt-cublas") == 0 && i8)                      ? 3
+                                                                               : 0;
+    if (c->gram_mode >= 2) c->gram_slices = 10;
+  }
+  if (const char* e = getenv("KST_GRAM_SLICES"))
+    c->gram_slices = c->gram_mode >= 2 ? std::min(14, std::max(8, atoi(e)))
+                                       : std::min(8, std::max(3, atoi(e)));
   DeviceGuard g(device);
   cudaFree(nullptr);  // establish the primary context
   *out = c;
@@ -126,13 +135,17 @@ long long kst_launch_count(const kst_ctx* ctx) { return ctx ? ctx->launches : -1
 
 int kst_set_gram(kst_ctx* ctx, int mode, int slices) {
   if (!ctx) return KST_ERR_DIMENSION;
-  if (mode != 0 && mode != 1) return set_err(ctx, KST_ERR_DIMENSION, "gram mode must be 0 or 1");
+  if (mode < 0 || mode > 3) return set_err(ctx, KST_ERR_DIMENSION, "gram mode must be 0..3");
   if (mode == 1 && (slices < 3 || slices > 8))
     return set_err(ctx, KST_ERR_DIMENSION, "int8 Gram needs 3..8 slices, got %d", slices);
-  if (mode == 1 && !kst::ozaki_available())
+  if (mode == 2 && !kst::crt_tc_available())
+    return set_err(ctx, KST_ERR_CUDA, "tcgen05 CRT Gram unavailable: no cuTensorMapEncodeTiled");
+  if (mode >= 2 && (slices < 8 || slices > 14))
+    return set_err(ctx, KST_ERR_DIMENSION, "CRT Gram needs 8..14 moduli, got %d", slices);
+  if (mode != 0 && !kst::ozaki_available())
     return set_err(ctx, KST_ERR_CUDA, "int8 Gram unavailable: cuBLAS not loadable");
   ctx->gram_mode = mode;
-  if (mode == 1) ctx->gram_slices = slices;
+  if (mode != 0) ctx->gram_slices = slices;
   return KST_OK;
 }
 

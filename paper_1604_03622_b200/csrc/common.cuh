@@ -66,7 +66,9 @@ struct kst_ctx {
   void* cusolver = nullptr;  // cusolverDnHandle_t, created lazily (heig.cu fallback)
   void* cublas = nullptr;    // cublasHandle_t for the int8 Gram (gram_ozaki.cu)
   // K1 engine: 0 = FP64 DMMA tiles (gram.cu), 1 = int8 tensor-core slices
-  // (gram_ozaki.cu) with `gram_slices` 7-bit slices per operand
+  // (gram_ozaki.cu) with `gram_slices` 7-bit slices per operand, 2 = int8
+  // modular residues (gram_crt.cu) with `gram_slices` moduli on the hand-written
+  // tcgen05 kernel, 3 = the same CRT numerics with cuBLAS int8 GEMMs
   int gram_mode = 0;
   int gram_slices = 7;
   double last_int8_ops = 0.0;  // int8 ops issued by the last int8 Gram (bench roofline)
@@ -210,6 +212,12 @@ int scm(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, cudaStream_t
 // gram_ozaki.cu
 bool ozaki_available();
 int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s, cudaStream_t st);
+// gram_crt.cu: modular (CRT) int8 Gram with `nmod` moduli (8..16); crt_beta
+// is the integer scaling it uses for n snapshots (-1 if unsupported)
+int scm_crt(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod, bool use_tc,
+            cudaStream_t st);
+bool crt_tc_available();  // cuTensorMapEncodeTiled reachable (tcgen05 path)
+int crt_beta(int nmod, int64_t n);
 // heig.cu
 struct TopEig {
   int r = 0;

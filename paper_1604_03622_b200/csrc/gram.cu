@@ -179,6 +179,8 @@ namespace kst {
 int scm(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, cudaStream_t st) {
   if (n < 1 || d < 1) return set_err(ctx, KST_ERR_DIMENSION, "scm: need n >= 1 and d >= 1");
   if (ctx->gram_mode == 1) return scm_ozaki(ctx, X, n, d, S, ctx->gram_slices, st);
+  if (ctx->gram_mode == 2 || ctx->gram_mode == 3)
+    return scm_crt(ctx, X, n, d, S, ctx->gram_slices, ctx->gram_mode == 2, st);
   const int64_t npad = ((n + BK - 1) / BK) * BK;
   const int64_t dpad = ((d + BM - 1) / BM) * BM;
   double* planes = (double*)ws_get(ctx, WS_PREP, sizeof(double) * 4 * npad * dpad);

@@ -1,0 +1,862 @@
+// K1 on the int8 tensor cores, modular form: the complex Gram
+// S = (1/n) X^T conj(X) (`sample_covariance`, src/lrkron.py:53-78) by the
+// Chinese remainder theorem over int8 residues (the "Ozaki scheme II" idea).
+//
+// Each column a is scaled by 2^(beta - E_a) (|x| < 2^E_a) and rounded to
+// integers x' (|x'| <= 2^beta, real and imaginary parts separately). For N
+// pairwise-coprime moduli m_i <= 256 (product P) the residues x' mod m_i fit
+// int8, so per modulus two int8 GEMMs give exact int32 products
+//     Re_i = [Xr Xi]^T [Xr Xi]   (K-stacked, depth 2n)      M_i = Xi^T Xr   (depth n)
+// and the exact integer Gram entries follow from
+//     V = sum_i c_i w_i - k P,   w_i = (P/m_i) ((P/m_i)^-1 mod m_i) < P,
+//     c_i = Re_i mod m_i    (Im: c_i = (M_i[a,b] - M_i[b,a]) mod m_i),
+//     k = round(sum_i c_i w_i / P) = round(sum_i c_i y_i / m_i)   (FP32 suffices).
+// beta is the largest value with 2n 2^(2 beta) <= P/4, so |V| <= P/4 and V is
+// the exact integer product; w_i and P are cut into 39-bit chunks so every
+// chunk sum is exact in FP64 and V costs two roundings. The only error is
+// rounding x to beta bits: ~n 2^-beta of max|x_a| max|x_b| (13 moduli,
+// n = 2001: beta = 44, vs 42 kept bits for 6 slices). N moduli cost 3N units
+// of int8 GEMM depth-n work against 3 s(s+1)/2 for s slices (13 vs 21 at s = 6).
+//
+// S is exactly Hermitian with a real diagonal (Im V[a,a] = 0 by construction);
+// non-finite columns poison their S entries with NaN (DataError upstream).
+#include <cuda.h>  // CUtensorMap types; the encoder is fetched with cudaGetDriverEntryPoint
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "gram_i8.cuh"
+
+namespace {
+
+using kst::i8::kNaNExpo;
+
+constexpr int kMaxMod = 16;  // table size; 3 x 39-bit chunks bound the product P < 2^117: <= 14 used
+constexpr int kMaxUsed = 14;
+// pairwise coprime: 2^8, 3.5.17, 11.23, 251, 13.19, 241, 239, 233, 229, 227,
+// 223, 7.31, 211, 199, 197, 193
+constexpr int kModuli[kMaxMod] = {256, 255, 253, 251, 247, 241, 239, 233,
+                                  229, 227, 223, 217, 211, 199, 197, 193};
+// device-side view (a select chain that folds to a constant in unrolled loops)
+__host__ __device__ constexpr int modulus(int i) {
+  return i == 0 ? 256 : i == 1 ? 255 : i == 2 ? 253 : i == 3 ? 251 : i == 4 ? 247 : i == 5 ? 241
+       : i == 6 ? 239 : i == 7 ? 233 : i == 8 ? 229 : i == 9 ? 227 : i == 10 ? 223 : i == 11 ? 217
+       : i == 12 ? 211 : i == 13 ? 199 : i == 14 ? 197 : 193;
+}
+
+struct CrtConst {
+  double w[kMaxMod][3];  // w_i = (w0 2^39 + w1) 2^39 + w2, chunks < 2^39
+  double p[3];           // P, same chunks
+  float ym[kMaxMod];     // y_i / m_i
+};
+__constant__ CrtConst c_crt;
+
+// ---------------------------------------------------------------- residues
+// R[a][i][part][k] = x'[k,a] mod m_i (part 0 real, 1 imag), centred in
+// [-(m-1)/2, (m-1)/2] for odd m and two's complement [-128, 127] for 256.
+// CTA = 16 columns x 64 rows; phase 1 reads X coalesced over a and cuts each
+// element into its 2N residue bytes (smem [i][part][a][k]); phase 2 writes
+// every (a, i, part) row segment with 4-byte stores coalesced over k.
+constexpr int CR_A = 16, CR_K = 64, CR_KP = CR_K + 4;
+template <int NM>
+__global__ void __launch_bounds__(256) crt_residue_kernel(
+    const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d, int64_t dpad,
+    const int* __restrict__ expo, int beta, int8_t* __restrict__ R) {
+  __shared__ __align__(16) int8_t sb[NM][2][CR_A][CR_KP];
+  const int64_t k0 = (int64_t)blockIdx.y * CR_K, a0 = (int64_t)blockIdx.x * CR_A;
+  const int tid = threadIdx.x;
+  {
+    const int c = tid & (CR_A - 1);
+    const int64_t a = a0 + c;
+    const int e = a < d ? expo[a] : 0;
+    const double sc = (e == kNaNExpo) ? 0.0 : ldexp(1.0, beta - e);
+    for (int r = tid / CR_A; r < CR_K; r += 256 / CR_A) {
+      const int64_t k = k0 + r;
+      const cplx v = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+      const double xr = rint(v.x * sc), xi = rint(v.y * sc);  // exact, |.| <= 2^beta
+      sb[0][0][c][r] = (int8_t)(long long)xr;                  // mod 256: low byte
+      sb[0][1][c][r] = (int8_t)(long long)xi;
+#pragma unroll
+      for (int i = 1; i < NM; ++i) {
+        // |x'| <= 2^48 keeps x' / m within 1/(16 m) of its double product, so
+        // rint picks the exact nearest quotient and the residue is centred
+        const double md = (double)modulus(i), inv = 1.0 / (double)modulus(i);
+        sb[i][0][c][r] = (int8_t)(int)fma(-md, rint(xr * inv), xr);
+        sb[i][1][c][r] = (int8_t)(int)fma(-md, rint(xi * inv), xi);
+      }
+    }
+  }
+  __syncthreads();
+  const int lw = tid & 15;
+  const int64_t k = k0 + 4 * lw;
+  if (k >= npad) return;  // npad is a multiple of 16: whole words only
+  for (int seg = tid >> 4; seg < CR_A * NM * 2; seg += 16) {
+    const int cc = seg / (2 * NM), rem = seg % (2 * NM), i = rem >> 1, part = rem & 1;
+    const int64_t a = a0 + cc;
+    if (a >= dpad) continue;
+    *(uint32_t*)(R + (((size_t)a * NM + i) * 2 + part) * npad + k) =
+        *(const uint32_t*)&sb[i][part][cc][4 * lw];
+  }
+}
+
+// ---------------------------------------------------------------- reconstruction
+// chunk sums (s0, s1, s2) and the FP32 quotient estimate -> V (two roundings)
+__device__ __forceinline__ double crt_finish(double s0, double s1, double s2, float kf) {
+  const double k = (double)rintf(kf);
+  s0 = fma(-k, c_crt.p[0], s0);  // exact: |k P_j| < 2^51, |result| < 2^52
+  s1 = fma(-k, c_crt.p[1], s1);
+  s2 = fma(-k, c_crt.p[2], s2);
+  const double t = fma(s0, 549755813888.0, s1);  // 2^39
+  return fma(t, 549755813888.0, s2);
+}
+
+// S from the per-modulus int32 products (column-major, ld = dpad): CTA per
+// (bi <= bj) pair of 32x32 tiles, writes S[a][b] and S[b][a] = conj.
+template <int NM>
+__global__ void __launch_bounds__(256, 2) crt_combine_kernel(
+    const int32_t* __restrict__ GRe, const int32_t* __restrict__ GM, int64_t dpad, int64_t d,
+    const int* __restrict__ expo, int beta, double dn, int T, cplx* __restrict__ S) {
+  __shared__ uint8_t mt[NM][32][33];  // mt[i][j][l] = M_i[b0+j][a0+l] mod m_i
+  __shared__ cplx vt[32][33];         // vt[j][l] = S[a0+j][b0+l]
+  const int t = blockIdx.x;
+  double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * t;
+  int bi = (int)floor(((2.0 * T + 1.0) - sqrt(disc)) * 0.5);
+  if (bi < 0) bi = 0;
+  while (bi > 0 && bi * T - bi * (bi - 1) / 2 > t) --bi;
+  while ((bi + 1) * T - (bi + 1) * bi / 2 <= t) ++bi;
+  const int bj = bi + (t - (bi * T - bi * (bi - 1) / 2));
+  const int64_t a0 = (int64_t)bi * 32, b0 = (int64_t)bj * 32;
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;
+  const int q4 = 4 * (tid & 7), r = tid >> 3;
+  const size_t plane = (size_t)dpad * dpad;
+  {  // transposed M block residues
+    const size_t idx = (size_t)(b0 + q4) + (size_t)(a0 + r) * dpad;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      const int m = modulus(i);
+      const int4 v = *(const int4*)(GM + (size_t)i * plane + idx);
+      const int u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int rr = u[c] % m;
+        mt[i][q4 + c][r] = (uint8_t)(rr < 0 ? rr + m : rr);
+      }
+    }
+  }
+  __syncthreads();
+  {
+    const int64_t b = b0 + r;
+    const size_t idx = (size_t)(a0 + q4) + (size_t)b * dpad;
+    double re0[4], re1[4], re2[4], im0[4], im1[4], im2[4];
+    float rek[4], imk[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
+      rek[c] = imk[c] = 0.0f;
+    }
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      const int m = modulus(i);
+      const int4 vr = *(const int4*)(GRe + (size_t)i * plane + idx);
+      const int4 vm = *(const int4*)(GM + (size_t)i * plane + idx);
+      const int ur[4] = {vr.x, vr.y, vr.z, vr.w}, um[4] = {vm.x, vm.y, vm.z, vm.w};
+      const double w0 = c_crt.w[i][0], w1 = c_crt.w[i][1], w2 = c_crt.w[i][2];
+      const float ym = c_crt.ym[i];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int cre = ur[c] % m;  // (-m, m)
+        int cim = um[c] % m;
+        cim = (cim < 0 ? cim + m : cim) - (int)mt[i][r][q4 + c];  // (-m, m)
+        const double dre = (double)cre, dim = (double)cim;
+        re0[c] = fma(dre, w0, re0[c]);
+        re1[c] = fma(dre, w1, re1[c]);
+        re2[c] = fma(dre, w2, re2[c]);
+        im0[c] = fma(dim, w0, im0[c]);
+        im1[c] = fma(dim, w1, im1[c]);
+        im2[c] = fma(dim, w2, im2[c]);
+        rek[c] = fmaf((float)cre, ym, rek[c]);
+        imk[c] = fmaf((float)cim, ym, imk[c]);
+      }
+    }
+    const int eb = (b < d) ? expo[b] : 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int64_t a = a0 + q4 + c;
+      const int ea = (a < d) ? expo[a] : 0;
+      cplx v;
+      if (ea == kNaNExpo || eb == kNaNExpo) {
+        v = cmk(NAN, NAN);
+      } else {
+        const double vre = crt_finish(re0[c], re1[c], re2[c], rek[c]);
+        const double vim = crt_finish(im0[c], im1[c], im2[c], imk[c]);
+        const int sh = ea + eb - 2 * beta;
+        v = cmk(ldexp(vre, sh) / dn, ldexp(vim, sh) / dn);
+      }
+      vt[q4 + c][r] = v;
+    }
+  }
+  __syncthreads();
+  for (int rr = ty; rr < 32; rr += 8) {
+    {  // S[a0 + rr][b0 + tx]
+      const int64_t a = a0 + rr, b = b0 + tx;
+      if (a < d && b < d && (bi != bj || a <= b)) {
+        const cplx v = vt[rr][tx];
+        S[a * d + b] = (a == b) ? cmk(v.x, 0.0) : v;
+      }
+    }
+    {  // S[b0 + rr][a0 + tx] = conj(S[a0 + tx][b0 + rr])
+      const int64_t b = b0 + rr, a = a0 + tx;
+      if (a < d && b < d && (bi != bj || a < b)) {
+        const cplx v = vt[tx][rr];
+        S[b * d + a] = cmk(v.x, -v.y);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host constants
+struct HostCrt {
+  int nmod = 0;
+  CrtConst c;
+  double log2p = 0.0;
+};
+
+int modinv(int a, int m) {  // a^-1 mod m (a, m coprime)
+  int t = 0, nt = 1, r = m, nr = a % m;
+  while (nr) {
+    const int q = r / nr;
+    int tmp = t - q * nt;
+    t = nt;
+    nt = tmp;
+    tmp = r - q * nr;
+    r = nr;
+    nr = tmp;
+  }
+  return t < 0 ? t + m : t;
+}
+
+const HostCrt& host_crt(int nmod) {
+  static HostCrt cache[kMaxMod + 1];
+  HostCrt& h = cache[nmod];
+  if (h.nmod == nmod) return h;
+  typedef unsigned __int128 u128;
+  u128 P = 1;
+  double lp = 0.0;
+  for (int i = 0; i < nmod; ++i) {
+    P *= (u128)kModuli[i];
+    lp += std::log2((double)kModuli[i]);
+  }
+  const u128 mask = ((u128)1 << 39) - 1;
+  auto chunks = [&](u128 v, double* out) {
+    out[0] = (double)(unsigned long long)(v >> 78);
+    out[1] = (double)(unsigned long long)((v >> 39) & mask);
+    out[2] = (double)(unsigned long long)(v & mask);
+  };
+  for (int i = 0; i < kMaxMod; ++i) {
+    if (i < nmod) {
+      const int m = kModuli[i];
+      const u128 Q = P / (u128)m;
+      const int y = modinv((int)(Q % (u128)m), m);
+      chunks(Q * (u128)y, h.c.w[i]);
+      h.c.ym[i] = (float)((double)y / (double)m);
+    } else {
+      h.c.w[i][0] = h.c.w[i][1] = h.c.w[i][2] = 0.0;
+      h.c.ym[i] = 0.0f;
+    }
+  }
+  chunks(P, h.c.p);
+  h.log2p = lp;
+  h.nmod = nmod;
+  return h;
+}
+
+template <int NM>
+void launch_crt(const cplx* X, int64_t n, int64_t npad, int64_t d, int64_t dpad, const int* expo,
+                int beta, int8_t* R, cudaStream_t st) {
+  crt_residue_kernel<NM><<<dim3(cdiv(dpad, CR_A), cdiv(npad, CR_K)), 256, 0, st>>>(
+      X, n, npad, d, dpad, expo, beta, R);
+}
+template <int NM>
+void launch_combine(const int32_t* GRe, const int32_t* GM, int64_t dpad, int64_t d, const int* expo,
+                    int beta, double dn, cplx* S, cudaStream_t st) {
+  const int T = (int)(dpad / 32);
+  crt_combine_kernel<NM><<<(unsigned)(T * (T + 1) / 2), 256, 0, st>>>(GRe, GM, dpad, d, expo, beta,
+                                                                      dn, T, S);
+}
+
+// ============================================================================
+// Hand-written tcgen05 path (sm_100a): the per-modulus products and their
+// modular reduction in one persistent kernel, no int32 planes.
+//
+// Work unit: an upper-triangle tile (I <= J) of 128 x 128 Gram entries. Per
+// modulus i and K block (128 snapshots) one TMA stage brings four 16 KB
+// operand tiles into smem (128B-swizzled, K-major):
+//   Ar = Xr'_I, Ai = Xi'_I, Br = Xr'_J, Bi = Xi'_J       (residues mod m_i)
+// and the MMA thread issues 16 tcgen05.mma.kind::i8 (M = N = 128, K = 32)
+// into three TMEM accumulators (int32, 128 lanes x 384 columns):
+//   Re += Ar.Br + Ai.Bi,   M += Ai.Br,   MT += Ar.Bi      (Im = M - MT)
+// Every operand byte feeds two products (128 int8 MACs per smem byte, the
+// same intensity as a 256 x 256 two-SM GEMM tile). After the last K block
+// of a modulus the four epilogue warps drain TMEM (tcgen05.ld, one TMEM lane
+// = one Gram row per thread), reduce Re and M - MT mod m_i and store uint8
+// residues; the next modulus starts as soon as TMEM is read. A separate
+// kernel then runs the CRT reconstruction on the residues (20 bytes per
+// entry for 10 moduli instead of 120 bytes of int32 products).
+//
+// Warp roles (576 threads): warp 0 = TMA producer (one lane), warp 1 = TMEM
+// allocator + MMA issuer (one lane), warps 2-17 = epilogue (warp w reads TMEM
+// lanes 32 (w % 4) .. +31, columns 32 ((w - 2) / 4) .. +31). Pipelines: smem
+// full/empty mbarriers (TMA <-> MMA, 3 stages of 64 KB), TMEM full/empty
+// (MMA <-> epilogue).
+constexpr int TC_BM = 128;                   // tile edge (rows = TMEM lanes, cols = N)
+constexpr int TC_BK = 128;                   // K bytes per stage (one 128B swizzle row)
+constexpr int TC_STAGES = 3;
+constexpr int TC_OPER = TC_BM * TC_BK;       // 16 KB operand tile
+constexpr int TC_STAGE_BYTES = 4 * TC_OPER;  // Ar, Ai, Br, Bi
+constexpr int TC_THREADS = 576;            // 2 control warps + 16 epilogue warps
+constexpr int TC_EPI_THREADS = 512;
+constexpr int TC_TMEM_COLS = 512;            // Re | M | MT (3 x 128), power-of-2 allocation
+constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
+// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A/B signed int8
+// (bits 7-9, 10-12 = 1), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                              ((uint32_t)(TC_BM >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+
+__constant__ int c_tc_mod[kMaxMod];
+__constant__ uint32_t c_tc_magic[kMaxMod];  // ceil(2^39 / m), 2^31 for m = 256
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity))
+    if (clock64() - t0 > (1ll << 33)) asm volatile("trap;");  // ~4 s at 2 GHz
+}
+__device__ __forceinline__ void tma_load3(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
+                                          int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// K-major operand in the canonical 128B-swizzled layout: 8-row groups of
+// 1024 B (SBO), LBO unused (1), descriptor version 1, layout SWIZZLE_128B (2)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kTcIdesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// row-major enumeration of the upper triangle of a T x T tile grid
+__host__ __device__ __forceinline__ void upper_tile(int t, int T, int& I, int& J) {
+  double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * t;
+  int i = (int)floor(((2.0 * T + 1.0) - sqrt(disc)) * 0.5);
+  if (i < 0) i = 0;
+  while (i > 0 && i * T - i * (i - 1) / 2 > t) --i;
+  while ((i + 1) * T - (i + 1) * i / 2 <= t) ++i;
+  I = i;
+  J = i + (t - (i * T - i * (i - 1) / 2));
+}
+
+// v mod m in [0, m) for |v| < 2^27, integer pipes only (no conversions):
+// u = v + m 2^20 in [0, 2^29), q = floor(u / m) = umulhi(u, ceil(2^39 / m)) >> 7,
+// exact for u < 2^29 and 128 < m <= 256 (magic = 2^31 for m = 256).
+__device__ __forceinline__ uint32_t tc_mod(int v, int m, uint32_t magic) {
+  const uint32_t u = (uint32_t)(v + (m << 20));
+  return u - (uint32_t)m * (__umulhi(u, magic) >> 7);
+}
+
+// res[t][i][comp][row][col] (uint8; comp 0 = Re, 1 = Im), t = upper tile index
+__global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
+    const __grid_constant__ CUtensorMap tmap, int T, int ntiles, int nmod, int nkb,
+    uint8_t* __restrict__ res) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(base + TC_STAGES * TC_STAGE_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = (uint32_t*)(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, TC_EPI_THREADS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "n"(TC_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int I, J;
+        upper_tile(t, T, I, J);
+        for (int i = 0; i < nmod; ++i)
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % TC_STAGES;
+            const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            uint8_t* st = base + s * TC_STAGE_BYTES;
+            mbar_expect_tx(&full[s], TC_STAGE_BYTES);
+            tma_load3(&tmap, &full[s], st, kb * TC_BK, 2 * i, I * TC_BM);
+            tma_load3(&tmap, &full[s], st + TC_OPER, kb * TC_BK, 2 * i + 1, I * TC_BM);
+            tma_load3(&tmap, &full[s], st + 2 * TC_OPER, kb * TC_BK, 2 * i, J * TC_BM);
+            tma_load3(&tmap, &full[s], st + 3 * TC_OPER, kb * TC_BK, 2 * i + 1, J * TC_BM);
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      int it = 0, pass = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int i = 0; i < nmod; ++i, ++pass) {
+          mbar_wait(tempty, ((uint32_t)pass & 1u) ^ 1u);  // epilogue drained TMEM
+          tc_fence_after();
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % TC_STAGES;
+            const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 32; ++kk) {
+              const uint64_t ar = sw128_desc(sa + 32 * kk);
+              const uint64_t ai = sw128_desc(sa + TC_OPER + 32 * kk);
+              const uint64_t br = sw128_desc(sa + 2 * TC_OPER + 32 * kk);
+              const uint64_t bi = sw128_desc(sa + 3 * TC_OPER + 32 * kk);
+              const uint32_t acc = (kb | kk) ? 1u : 0u;
+              tc_mma_i8(tmem, ar, br, acc);          // Re  = Xr_a Xr_b
+              tc_mma_i8(tmem, ai, bi, 1u);           //     + Xi_a Xi_b
+              tc_mma_i8(tmem + 128, ai, br, acc);    // M   = Xi_a Xr_b
+              tc_mma_i8(tmem + 256, ar, bi, acc);    // MT  = Xr_a Xi_b
+            }
+            tc_commit(&empty[s]);  // smem slot reusable once these MMAs retire
+          }
+          tc_commit(tfull);  // accumulators of modulus i complete
+        }
+    }
+  } else {  // ---------------- epilogue: TMEM -> residues
+    // 16 warps: lane quarter q = warp % 4 (TMEM lanes 32q..32q+31 = tile rows),
+    // column block cb = (warp - 2) / 4 (32 of the 128 columns). Each thread
+    // loads its 32 Re, M and MT words, releases TMEM, and only then reduces
+    // and stores, so the next modulus' MMAs overlap the modular arithmetic.
+    const int q = warp & 3, cb = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + 32 * cb;
+    int pass = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int i = 0; i < nmod; ++i, ++pass) {
+        mbar_wait(tfull, (uint32_t)pass & 1u);
+        tc_fence_after();
+        uint32_t vre[32], vm[32], vmt[32];
+        tc_ld32(taddr, vre);
+        tc_ld32(taddr + 128, vm);
+        tc_ld32(taddr + 256, vmt);
+        tc_wait_ld();
+        tc_fence_before();
+        mbar_arrive(tempty);  // TMEM free for modulus i + 1
+        const int m = c_tc_mod[i];
+        const uint32_t magic = c_tc_magic[i];
+        uint32_t pre[8], pim[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          uint32_t a = 0, b = 0;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = 4 * w + e;
+            a |= tc_mod((int)vre[j], m, magic) << (8 * e);
+            b |= tc_mod((int)vm[j] - (int)vmt[j], m, magic) << (8 * e);
+          }
+          pre[w] = a;
+          pim[w] = b;
+        }
+        uint8_t* out_re = res + (((size_t)t * nmod + i) * 2) * (TC_BM * TC_BM) +
+                          (size_t)row * TC_BM + 32 * cb;
+        uint4* dre = (uint4*)out_re;
+        uint4* dim = (uint4*)(out_re + TC_BM * TC_BM);
+        dre[0] = make_uint4(pre[0], pre[1], pre[2], pre[3]);
+        dre[1] = make_uint4(pre[4], pre[5], pre[6], pre[7]);
+        dim[0] = make_uint4(pim[0], pim[1], pim[2], pim[3]);
+        dim[1] = make_uint4(pim[4], pim[5], pim[6], pim[7]);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(TC_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// CRT reconstruction from the uint8 residue tiles: CTA per (tile, 32 x 32
+// sub-block); writes S[a][b] and the conjugate mirror S[b][a] (coalesced via
+// an smem transpose). Diagonal tiles keep a <= b only.
+template <int NM>
+__global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
+    const uint8_t* __restrict__ res, int T, const int* __restrict__ expo, int beta, double dn,
+    int64_t d, cplx* __restrict__ S) {
+  __shared__ cplx vt[32][33];
+  const int t = blockIdx.x >> 4, sb = blockIdx.x & 15;
+  int I, J;
+  upper_tile(t, T, I, J);
+  const int sr = sb >> 2, sc = sb & 3;
+  const int tid = threadIdx.x;
+  const int q4 = 4 * (tid & 7), r = tid >> 3;
+  const int lr = 32 * sr + r, lc = 32 * sc + q4;  // tile-local row / first column
+  const int64_t a = (int64_t)I * TC_BM + lr;
+  double re0[4], re1[4], re2[4], im0[4], im1[4], im2[4];
+  float rek[4], imk[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
+    rek[c] = imk[c] = 0.0f;
+  }
+  const uint8_t* src = res + (size_t)t * NM * 2 * (TC_BM * TC_BM) + (size_t)lr * TC_BM + lc;
+  uint32_t pr[NM], pm[NM];
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    pr[i] = *(const uint32_t*)(src + (size_t)(2 * i) * (TC_BM * TC_BM));
+    pm[i] = *(const uint32_t*)(src + (size_t)(2 * i + 1) * (TC_BM * TC_BM));
+  }
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const double w0 = c_crt.w[i][0], w1 = c_crt.w[i][1], w2 = c_crt.w[i][2];
+    const float ym = c_crt.ym[i];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t cr = (pr[i] >> (8 * c)) & 0xFFu, cm = (pm[i] >> (8 * c)) & 0xFFu;
+      // byte -> double / float by exponent splicing (FP64 / FP32 pipes, not the
+      // conversion unit): 2^52 + c - 2^52, 2^23 + c - 2^23
+      const double dr = __longlong_as_double(0x4330000000000000ll | cr) - 4503599627370496.0;
+      const double dm = __longlong_as_double(0x4330000000000000ll | cm) - 4503599627370496.0;
+      const float fr = __int_as_float(0x4B000000 | (int)cr) - 8388608.0f;
+      const float fm = __int_as_float(0x4B000000 | (int)cm) - 8388608.0f;
+      re0[c] = fma(dr, w0, re0[c]);
+      re1[c] = fma(dr, w1, re1[c]);
+      re2[c] = fma(dr, w2, re2[c]);
+      im0[c] = fma(dm, w0, im0[c]);
+      im1[c] = fma(dm, w1, im1[c]);
+      im2[c] = fma(dm, w2, im2[c]);
+      rek[c] = fmaf(fr, ym, rek[c]);
+      imk[c] = fmaf(fm, ym, imk[c]);
+    }
+  }
+  const int ea = (a < d) ? expo[a] : 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int64_t b = (int64_t)J * TC_BM + lc + c;
+    const int eb = (b < d) ? expo[b] : 0;
+    cplx v;
+    if (ea == kNaNExpo || eb == kNaNExpo) {
+      v = cmk(NAN, NAN);
+    } else {
+      const double vre = crt_finish(re0[c], re1[c], re2[c], rek[c]);
+      const double vim = crt_finish(im0[c], im1[c], im2[c], imk[c]);
+      const int sh = ea + eb - 2 * beta;
+      v = cmk(ldexp(vre, sh) / dn, ldexp(vim, sh) / dn);
+    }
+    vt[r][q4 + c] = v;
+  }
+  __syncthreads();
+  const int tx = tid & 31, ty = tid >> 5;
+  const int64_t a0 = (int64_t)I * TC_BM + 32 * sr, b0 = (int64_t)J * TC_BM + 32 * sc;
+  for (int rr = ty; rr < 32; rr += 8) {
+    {  // S[a0 + rr][b0 + tx]
+      const int64_t aa = a0 + rr, bb = b0 + tx;
+      if (aa < d && bb < d && aa <= bb) {
+        const cplx v = vt[rr][tx];
+        S[aa * d + bb] = (aa == bb) ? cmk(v.x, 0.0) : v;
+      }
+    }
+    {  // S[b0 + rr][a0 + tx] = conj(S[a0 + tx][b0 + rr])
+      const int64_t bb = b0 + rr, aa = a0 + tx;
+      if (aa < d && bb < d && aa < bb) {
+        const cplx v = vt[tx][rr];
+        S[bb * d + aa] = cmk(v.x, -v.y);
+      }
+    }
+  }
+}
+
+template <int NM>
+void launch_tile_combine(const uint8_t* res, int T, int ntiles, const int* expo, int beta, double dn,
+                         int64_t d, cplx* S, cudaStream_t st) {
+  crt_tile_combine_kernel<NM><<<(unsigned)ntiles * 16, 256, 0, st>>>(res, T, expo, beta, dn, d, S);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+#define KST_CRT_DISPATCH(NMV, CALL)                \
+  switch (NMV) {                                   \
+    case 8: { constexpr int NM_ = 8; CALL; } break;   \
+    case 9: { constexpr int NM_ = 9; CALL; } break;   \
+    case 10: { constexpr int NM_ = 10; CALL; } break; \
+    case 11: { constexpr int NM_ = 11; CALL; } break; \
+    case 12: { constexpr int NM_ = 12; CALL; } break; \
+    case 13: { constexpr int NM_ = 13; CALL; } break; \
+    default: { constexpr int NM_ = 14; CALL; } break; \
+  }
+
+}  // namespace
+
+namespace kst {
+
+int crt_beta(int nmod, int64_t n) {
+  if (nmod < 8 || nmod > kMaxUsed || n < 1) return -1;
+  const double lp = host_crt(nmod).log2p;
+  // 2n 2^(2 beta) <= P / 4 (exact products, |V| <= P/4); small safety margin
+  const int beta = (int)std::floor((lp - 3.0 - std::log2((double)n) - 1e-6) / 2.0);
+  return std::min(beta, 48);
+}
+
+bool crt_tc_available() { return encode_tiled() != nullptr; }
+
+// tcgen05 path: residues -> gram_tc_kernel (products + modular reduction) ->
+// crt_tile_combine_kernel (reconstruction). Caller validated nmod / n.
+static int scm_crt_tc(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod, int beta,
+                      cudaStream_t st) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return set_err(ctx, KST_ERR_CUDA, "scm_crt: cuTensorMapEncodeTiled unavailable");
+  const int64_t npad = ((n + 15) / 16) * 16;
+  const int64_t dpad = ((d + TC_BM - 1) / TC_BM) * TC_BM;
+  const int T = (int)(dpad / TC_BM);
+  const int ntiles = T * (T + 1) / 2;
+  const int nkb = (int)((npad + TC_BK - 1) / TC_BK);
+  const int64_t ldr = (int64_t)nmod * 2 * npad;
+  char* sl = (char*)ws_get(ctx, WS_OZ_SLICES, (size_t)dpad * ldr + sizeof(int) * dpad + 256);
+  uint8_t* res = (uint8_t*)ws_get(ctx, WS_OZ_PROD, (size_t)ntiles * nmod * 2 * TC_BM * TC_BM);
+  if (!sl || !res) return set_err(ctx, KST_ERR_CUDA, "scm_crt: workspace");
+  int8_t* R = (int8_t*)sl;
+  int* expo = (int*)(R + (size_t)dpad * ldr);
+  {
+    static int mods[kMaxMod];
+    static uint32_t magic[kMaxMod];
+    for (int i = 0; i < kMaxMod; ++i) {
+      mods[i] = kModuli[i];
+      magic[i] = kModuli[i] == 256 ? (1u << 31)
+                                   : (uint32_t)((((uint64_t)1 << 39) + kModuli[i] - 1) / kModuli[i]);
+    }
+    KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_tc_mod, mods, sizeof(mods), 0, cudaMemcpyHostToDevice, st));
+    KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_tc_magic, magic, sizeof(magic), 0, cudaMemcpyHostToDevice, st));
+  }
+  CUtensorMap map;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)npad, (cuuint64_t)(2 * nmod), (cuuint64_t)dpad};
+    const cuuint64_t strides[2] = {(cuuint64_t)npad, (cuuint64_t)ldr};  // bytes, dims 1 and 2
+    const cuuint32_t box[3] = {TC_BK, 1, TC_BM};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)R, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(ctx, KST_ERR_CUDA, "cuTensorMapEncodeTiled failed: %d", (int)r);
+  }
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = kNumSMs;
+  }
+  i8::colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
+  KST_LAUNCH(ctx);
+  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, st)));
+  KST_LAUNCH(ctx);
+  KST_CUDA(ctx, cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)TC_SMEM));
+  stage_mark(ctx, 5, st);  // profiling: int8 tensor-core span (events 5..6)
+  gram_tc_kernel<<<(unsigned)std::min(ntiles, nsm), TC_THREADS, TC_SMEM, st>>>(map, T, ntiles, nmod,
+                                                                              nkb, res);
+  KST_LAUNCH(ctx);
+  stage_mark(ctx, 6, st);
+  ctx->last_int8_ops = 2.0 * 4.0 * (double)TC_BM * TC_BM * (double)nkb * TC_BK * nmod * ntiles;
+  KST_CRT_DISPATCH(nmod, (launch_tile_combine<NM_>(res, T, ntiles, expo, beta, (double)n, d, S, st)));
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}
+
+int scm_crt(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod, bool use_tc,
+            cudaStream_t st) {
+  if (nmod < 8 || nmod > kMaxUsed)
+    return set_err(ctx, KST_ERR_DIMENSION, "CRT Gram needs 8..%d moduli, got %d", kMaxUsed, nmod);
+  const int beta = crt_beta(nmod, n);
+  if (beta < 8) return set_err(ctx, KST_ERR_DIMENSION, "CRT Gram: n=%lld too large for %d moduli",
+                               (long long)n, nmod);
+  if (2 * n > (int64_t)1 << 17)
+    return set_err(ctx, KST_ERR_DIMENSION, "CRT Gram: int32 products need n <= 65536");
+  const HostCrt& hc = host_crt(nmod);
+  KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_crt, &hc.c, sizeof(CrtConst), 0, cudaMemcpyHostToDevice, st));
+  if (use_tc) return scm_crt_tc(ctx, X, n, d, S, nmod, beta, st);
+  if (!i8::load_blas()) return set_err(ctx, KST_ERR_CUDA, "scm_crt: cuBLAS not loadable");
+  cublasHandle_t h = i8::blas_handle(ctx, st);
+  if (!h) return set_err(ctx, KST_ERR_CUDA, "cublasCreate failed");
+
+  const int64_t npad = ((n + 15) / 16) * 16;
+  constexpr int NB = 4;  // Re is symmetric: upper blocks of an NB x NB grid
+  const bool blocked = d >= 1024;
+  const int64_t dpad = blocked ? ((d + 32 * NB - 1) / (32 * NB)) * (32 * NB) : ((d + 31) / 32) * 32;
+  const int64_t bsz = dpad / NB;
+  constexpr int NBLK = NB * (NB + 1) / 2;
+  const size_t plane = (size_t)dpad * dpad;
+  const int64_t ldr = (int64_t)nmod * 2 * npad;  // bytes per column a
+  char* sl = (char*)ws_get(ctx, WS_OZ_SLICES, (size_t)dpad * ldr + sizeof(int) * dpad +
+                                                   sizeof(void*) * 3 * NBLK * kMaxMod + 512);
+  int32_t* G = (int32_t*)ws_get(ctx, WS_OZ_PROD, sizeof(int32_t) * 2 * nmod * plane);
+  if (!sl || !G) return set_err(ctx, KST_ERR_CUDA, "scm_crt: workspace");
+  int8_t* R = (int8_t*)sl;
+  int* expo = (int*)(R + (size_t)dpad * ldr);
+  void** dptr = (void**)(((uintptr_t)(expo + dpad) + 255) & ~(uintptr_t)255);
+  int32_t* GRe = G;
+  int32_t* GM = G + (size_t)nmod * plane;
+  if (blocked) {
+    void** hp = (void**)pinned_get(ctx, sizeof(void*) * 3 * NBLK * kMaxMod);
+    if (!hp) return set_err(ctx, KST_ERR_CUDA, "scm_crt: pinned staging");
+    // [A | B | C] pointer arrays, each nmod x NBLK
+    for (int i = 0; i < nmod; ++i) {
+      int k = 0;
+      for (int I = 0; I < NB; ++I)
+        for (int J = I; J < NB; ++J, ++k) {
+          const size_t e = (size_t)i * NBLK + k;
+          hp[e] = (void*)(R + (size_t)i * 2 * npad + (size_t)I * bsz * ldr);
+          hp[(size_t)nmod * NBLK + e] = (void*)(R + (size_t)i * 2 * npad + (size_t)J * bsz * ldr);
+          hp[(size_t)2 * nmod * NBLK + e] =
+              (void*)(GRe + (size_t)i * plane + I * bsz + (size_t)J * bsz * dpad);
+        }
+    }
+    KST_CUDA(ctx, cudaMemcpyAsync(dptr, hp, sizeof(void*) * 3 * NBLK * nmod, cudaMemcpyHostToDevice, st));
+  }
+  i8::colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
+  KST_LAUNCH(ctx);
+  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, st)));
+  KST_LAUNCH(ctx);
+  stage_mark(ctx, 5, st);  // profiling: int8 GEMM span (events 5..6)
+  const int32_t one = 1, zero = 0;
+  for (int i = 0; i < nmod; ++i) {
+    const int8_t* Ri = R + (size_t)i * 2 * npad;
+    cublasStatus_t r1;
+    if (blocked) {
+      void** A = dptr + (size_t)i * NBLK;
+      void** B = dptr + (size_t)(nmod + i) * NBLK;
+      void** Cc = dptr + (size_t)(2 * nmod + i) * NBLK;
+      r1 = i8::g_blas.gemm_batched_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)bsz, (int)bsz, (int)(2 * npad),
+                                      &one, (const void* const*)A, CUDA_R_8I, (int)ldr,
+                                      (const void* const*)B, CUDA_R_8I, (int)ldr, &zero, Cc,
+                                      CUDA_R_32I, (int)dpad, NBLK, CUBLAS_COMPUTE_32I,
+                                      CUBLAS_GEMM_DEFAULT);
+    } else {
+      r1 = i8::g_blas.gemm_ex(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)dpad, (int)dpad, (int)(2 * npad), &one,
+                              Ri, CUDA_R_8I, (int)ldr, Ri, CUDA_R_8I, (int)ldr, &zero,
+                              GRe + (size_t)i * plane, CUDA_R_32I, (int)dpad, CUBLAS_COMPUTE_32I,
+                              CUBLAS_GEMM_DEFAULT);
+    }
+    // M_i[a][b] = sum_k Xi'[k,a] Xr'[k,b] (mod-m_i residues)
+    const cublasStatus_t r2 = i8::g_blas.gemm_ex(
+        h, CUBLAS_OP_T, CUBLAS_OP_N, (int)dpad, (int)dpad, (int)npad, &one, Ri + npad, CUDA_R_8I,
+        (int)ldr, Ri, CUDA_R_8I, (int)ldr, &zero, GM + (size_t)i * plane, CUDA_R_32I, (int)dpad,
+        CUBLAS_COMPUTE_32I, CUBLAS_GEMM_DEFAULT);
+    if (r1 != CUBLAS_STATUS_SUCCESS || r2 != CUBLAS_STATUS_SUCCESS)
+      return set_err(ctx, KST_ERR_CUDA, "cublasGemmEx (int8 CRT) failed: %d %d", (int)r1, (int)r2);
+    ctx->launches += 2;
+  }
+  stage_mark(ctx, 6, st);
+  {
+    const double re_frac = blocked ? (double)NBLK / (NB * NB) : 1.0;
+    ctx->last_int8_ops = 2.0 * (double)dpad * (double)dpad * (double)npad * nmod * (2.0 * re_frac + 1.0);
+  }
+  KST_CRT_DISPATCH(nmod, (launch_combine<NM_>(GRe, GM, dpad, d, expo, beta, (double)n, S, st)));
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}
+
+}  // namespace kst

@@ -19,17 +19,14 @@
 // the B200 tensor cores, bound with dlopen); slicing and recombination are
 // hand-written kernels. Non-finite columns poison their S entries with NaN so
 // the estimator's finite check raises DataError exactly like the FP64 path.
-#include <cublas_v2.h>  // types only: every cuBLAS entry point is bound with dlsym
 #include <dlfcn.h>
 
 #include <algorithm>
-#include <climits>
 
-#include "common.cuh"
+#include "gram_i8.cuh"
 
-namespace {
-
-constexpr int kNaNExpo = INT_MIN;
+namespace kst {
+namespace i8 {
 
 // E_a per column: smallest E with max_k max(|re|, |im|) < 2^E; NaN sentinel
 // for non-finite columns; 0 for all-zero columns (slices are then zero).
@@ -59,6 +56,14 @@ __global__ void colmax_kernel(const cplx* __restrict__ X, int64_t n, int64_t d,
     expo[a] = bad ? kNaNExpo : (m > 0.0 ? ilogb(m) + 1 : 0);
   }
 }
+
+}  // namespace i8
+}  // namespace kst
+
+namespace {
+
+using kst::i8::kNaNExpo;
+using kst::i8::colmax_kernel;
 
 // Slices, column-major per snapshot element a (K blocks of npad contiguous):
 //   RIf[a][2t + c][k] = sigma_{t+1}(part c)[k,a]       (c = 0 real, 1 imag)
@@ -225,21 +230,11 @@ __global__ void __launch_bounds__(256, 2) ozaki_combine_kernel(
   }
 }
 
+}  // namespace
+
+namespace kst {
+namespace i8 {
 // ---------------------------------------------------------------- cuBLAS binding
-struct Blas {
-  bool tried = false, ok = false;
-  cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
-  cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
-  cublasStatus_t (*gemm_ex)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
-                            const void*, const void*, cudaDataType, int, const void*, cudaDataType,
-                            int, const void*, void*, cudaDataType, int, cublasComputeType_t,
-                            cublasGemmAlgo_t) = nullptr;
-  cublasStatus_t (*gemm_batched_ex)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int,
-                                    int, const void*, const void* const[], cudaDataType, int,
-                                    const void* const[], cudaDataType, int, const void*,
-                                    void* const[], cudaDataType, int, int, cublasComputeType_t,
-                                    cublasGemmAlgo_t) = nullptr;
-};
 Blas g_blas;
 bool load_blas() {
   if (g_blas.tried) return g_blas.ok;
@@ -257,22 +252,28 @@ bool load_blas() {
   return g_blas.ok;
 }
 
-}  // namespace
+cublasHandle_t blas_handle(kst_ctx* ctx, cudaStream_t st) {
+  if (!ctx->cublas) {
+    cublasHandle_t h;
+    if (g_blas.create(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
+    ctx->cublas = (void*)h;
+  }
+  cublasHandle_t h = (cublasHandle_t)ctx->cublas;
+  g_blas.set_stream(h, st);
+  return h;
+}
 
-namespace kst {
+}  // namespace i8
+
+using i8::g_blas;
+using i8::load_blas;
 
 bool ozaki_available() { return load_blas(); }
 
 int scm_ozaki(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int s, cudaStream_t st) {
   if (!load_blas()) return set_err(ctx, KST_ERR_CUDA, "scm_ozaki: cuBLAS not loadable");
-  if (!ctx->cublas) {
-    cublasHandle_t h;
-    if (g_blas.create(&h) != CUBLAS_STATUS_SUCCESS)
-      return set_err(ctx, KST_ERR_CUDA, "cublasCreate failed");
-    ctx->cublas = (void*)h;
-  }
-  cublasHandle_t h = (cublasHandle_t)ctx->cublas;
-  g_blas.set_stream(h, st);
+  cublasHandle_t h = i8::blas_handle(ctx, st);
+  if (!h) return set_err(ctx, KST_ERR_CUDA, "cublasCreate failed");
   const int64_t npad = ((n + 15) / 16) * 16;  // K multiple of 16 (int8 tensor-op alignment)
   // Re = GR + GI is symmetric: for large d only the NB(NB+1)/2 upper blocks of
   // an NB x NB block grid are multiplied (one batched GEMM per diagonal e).

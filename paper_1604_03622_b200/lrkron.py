@@ -98,17 +98,21 @@ class KronCovEstimate:
 
 def set_gram_engine(mode="dmma", slices=7, device=None):
     """Select the sample-covariance engine (K1) for this thread's context:
-    "dmma" (FP64 tensor-core tiles) or "int8" (exact int8 slices on the int8
-    tensor cores, `slices` 7-bit slices per operand)."""
+    "dmma" (FP64 tensor-core tiles), "int8" (exact int8 slices on the int8
+    tensor cores, `slices` 7-bit slices per operand), "crt" (int8 modular
+    residues recombined by the Chinese remainder theorem, `slices` moduli, on
+    the hand-written tcgen05 kernel) or "crt-cublas" (same numerics, cuBLAS
+    int8 GEMMs)."""
     c = nat.ctx(device)
-    nat.check(nat.lib().kst_set_gram(c, {"dmma": 0, "int8": 1}[mode], int(slices)), c)
+    code = {"dmma": 0, "int8": 1, "crt": 2, "crt-cublas": 3}[mode]
+    nat.check(nat.lib().kst_set_gram(c, code, int(slices)), c)
 
 
 def get_gram_engine(device=None):
     c = nat.ctx(device)
     m, s = C.c_int(0), C.c_int(0)
     nat.check(nat.lib().kst_get_gram(c, C.byref(m), C.byref(s)), c)
-    return ("dmma", "int8")[m.value], s.value
+    return ("dmma", "int8", "crt", "crt-cublas")[m.value], s.value
 
 
 def _shape(x):

@@ -42,12 +42,14 @@ def _proj(u):
     return u @ u.conj().T
 
 
-@pytest.mark.parametrize("slices", [5, 6, 7])
-def test_gotcha_frame_matches_oracle(frame, slices):
+@pytest.mark.parametrize("engine", [("int8", 5), ("int8", 6), ("int8", 7), ("crt", 8), ("crt", 9),
+                                    ("crt", 10), ("crt", 11), ("crt", 12), ("crt", 14)])
+def test_gotcha_frame_matches_oracle(frame, engine):
     cube, fit, ua, ub, ref, m0 = frame
+    mode, slices = engine
     before = lrkron.get_gram_engine()
     try:
-        lrkron.set_gram_engine("int8", slices)
+        lrkron.set_gram_engine(mode, slices)
         scm = kst.sample_covariance(kst.cube_to_snapshots(cube), P, Q)
         est = kst.lr_kron_estimate(scm, RA, RB, tol=1e-4, max_iter=100)
         filt = kst.build_filter("kron", estimate=est)
@@ -64,7 +66,7 @@ def test_gotcha_frame_matches_oracle(frame, slices):
     err = np.abs(img.values - ref)
     ferr = np.abs(fused - ref)
     budget = map_tolerance(ref, m0)
-    print(f"\n[s={slices}] iters {est.iterations}/{fit.iterations} residual rel {res_err:.2e} "
+    print(f"\n[{mode} {slices}] iters {est.iterations}/{fit.iterations} residual rel {res_err:.2e} "
           f"spatial rel {sp_err:.2e} proj A {pa:.2e} proj B {pb:.2e} "
           f"map max err/M0 {err.max() / m0:.2e} (budget used {np.max(err / budget):.2e}) "
           f"fused/M0 {ferr.max() / m0:.2e}")
@@ -72,6 +74,6 @@ def test_gotcha_frame_matches_oracle(frame, slices):
     assert info["iterations"] == fit.iterations
     assert res_err <= 1e-9
     # s = 5 measured 9.7e-10 on this frame: the spatial factor gets one decade
-    assert sp_err <= (1e-9 if slices >= 6 else 1e-8)
+    assert sp_err <= (1e-9 if (mode, slices) != ("int8", 5) else 1e-8)
     assert pa < 1e-8 and pb < 1e-8
     assert np.all(err <= budget) and np.all(ferr <= budget)

@@ -229,11 +229,69 @@ def test_int8_gram_engine_error_bound(slices):
     assert np.linalg.norm(s - ref) <= bound * np.linalg.norm(ref)
 
 
-def test_int8_gram_propagates_non_finite_inputs():
+MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
+
+
+@pytest.mark.parametrize("nmod", [8, 9, 10, 12, 14])
+def test_crt_gram_engine_error_bound(nmod):
+    """The modular (CRT) int8 Gram against the FP64 DMMA Gram: exactly
+    Hermitian, real diagonal, error of rounding x to beta bits, where beta is
+    the largest value with 2n 2^(2 beta) <= P/4 (gram_crt.cu)."""
+    from paper_1604_03622_b200 import lrkron, scenes
+    n = 256
+    cube = scenes.bench_scene(3, 256, n, seed=17).data[0]
+    snaps = kst.cube_to_snapshots(cube)
+    before = lrkron.get_gram_engine()
+    try:
+        lrkron.set_gram_engine("dmma")
+        ref = kst.sample_covariance(snaps, 3, 256).matrix
+        lrkron.set_gram_engine("crt", nmod)
+        assert lrkron.get_gram_engine() == ("crt", nmod)
+        s = kst.sample_covariance(snaps, 3, 256).matrix
+    finally:
+        lrkron.set_gram_engine(*before)
+    log2p = sum(np.log2(MODULI[:nmod]))
+    beta = min(int(np.floor((log2p - 3 - np.log2(n) - 1e-6) / 2)), 48)
+    assert np.array_equal(s, s.conj().T)
+    assert not np.any(np.diagonal(s).imag)
+    dg = np.sqrt(np.outer(ref.diagonal().real, ref.diagonal().real))
+    bound = 64 * 2.0 ** (-beta)
+    assert (np.abs(s - ref) / dg).max() <= bound
+    assert np.linalg.norm(s - ref) <= bound * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("shape", [(3, 256, 256), (3, 100, 77), (2, 300, 1000), (1, 40, 3)])
+@pytest.mark.parametrize("nmod", [9, 10, 13])
+def test_crt_tcgen05_kernel_matches_library_gemm_path(shape, nmod):
+    """The hand-written tcgen05 CRT Gram (mode "crt") against the same CRT
+    numerics on cuBLAS int8 GEMMs (mode "crt-cublas"): both recover the same
+    exact integer products, so S agrees to the last rounding of the
+    reconstruction; ragged shapes exercise the TMA out-of-bounds fill."""
+    from paper_1604_03622_b200 import lrkron
+    p, q, n = shape
+    rng = np.random.default_rng(7 + n)
+    snaps = rng.standard_normal((n, p * q)) + 1j * rng.standard_normal((n, p * q))
+    snaps[:, 0] *= 1e3  # column scales differ
+    before = lrkron.get_gram_engine()
+    try:
+        lrkron.set_gram_engine("crt-cublas", nmod)
+        ref = kst.sample_covariance(snaps, p, q).matrix
+        lrkron.set_gram_engine("crt", nmod)
+        s = kst.sample_covariance(snaps, p, q).matrix
+    finally:
+        lrkron.set_gram_engine(*before)
+    assert np.array_equal(s, s.conj().T)
+    assert not np.any(np.diagonal(s).imag)
+    dg = np.sqrt(np.outer(ref.diagonal().real, ref.diagonal().real))
+    assert (np.abs(s - ref) / dg).max() <= 1e-14
+
+
+@pytest.mark.parametrize("engine", [("int8", 6), ("crt", 10), ("crt-cublas", 10)])
+def test_int8_gram_propagates_non_finite_inputs(engine):
     from paper_1604_03622_b200 import lrkron
     before = lrkron.get_gram_engine()
     try:
-        lrkron.set_gram_engine("int8", 6)
+        lrkron.set_gram_engine(*engine)
         x = np.ones((8, 6), complex)
         x[3, 2] = np.nan
         scm = kst.sample_covariance(x, 2, 3)

@@ -177,6 +177,29 @@ def int8_roofline(ops, gemm_ms, slices, flops, gram_ms):
                            "dense on B200); cuBLAS int8 measured 3.03 POPS here (tools/int8_probe.py)"}
 
 
+def crt_roofline(nmod, n, d, tc_ms, executed_ops, flops, gram_ms):
+    """Dominant kernel of the CRT engine: gram_tc_kernel (hand-written tcgen05,
+    int8 tensor cores). Algorithmic work: per modulus four real int8 products
+    (Re: XrXr + XiXi, Im: XiXr - XrXi) for each of the n d (d + 1) / 2 Hermitian
+    entries, 2 ops per MAC. Duration: CUDA events bracketing that one launch
+    (kst_stage_times entry 5). Peak: 2 x the measured dense bf16 rate in
+    MEASURED_PEAKS.json (int8 dense = 2 x bf16 dense on B200)."""
+    pk = measured_peaks()
+    peak = 2.0 * pk.get("bf16_tflops_sustained", 1376.6)
+    alg = 2.0 * 4.0 * nmod * n * d * (d + 1) / 2.0
+    traffic, _ = ncu_traffic("gram_tc_ncu.json")
+    achieved = alg / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else 0.0
+    return {"kernel": f"gram_tc_kernel (K1 CRT Gram, {nmod} moduli, tcgen05 kind::i8, TMA, TMEM)",
+            "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOP/s (int8)",
+            "frac": achieved / peak, "traffic": traffic,
+            "algorithmic": f"8*nmod*n*d(d+1)/2 = {alg:.4e} int8 ops per launch "
+                           f"({executed_ops:.4e} issued incl. 128-tile padding)",
+            "kernel_ms": tc_ms, "gram_stage_ms": gram_ms,
+            "fp64_equivalent_tflops": flops / (gram_ms * 1e-3) / 1e12,
+            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 dense = 2 x bf16 "
+                           "dense on B200)"}
+
+
 def cpu_threads():
     return os.cpu_count() or 1
 
@@ -328,6 +351,11 @@ def main():
         flops = 4.0 * n * float(p * q) ** 2          # Hermitian half, 8 flop per complex MAC
         engine, slices = kst.lrkron.get_gram_engine(dev)
         if engine == "int8":
+            roof = int8_roofline(lib.kst_gram_int8_ops(c), float(st[5]), slices, flops, gram_ms)
+        elif engine == "crt":
+            roof = crt_roofline(slices, n, p * q, float(st[5]), lib.kst_gram_int8_ops(c), flops,
+                                gram_ms)
+        elif engine == "crt-cublas":
             roof = int8_roofline(lib.kst_gram_int8_ops(c), float(st[5]), slices, flops, gram_ms)
         else:
             roof = fp64_roofline(flops, gram_ms)

@@ -92,18 +92,20 @@ int kst_ctx_create(int device, kst_ctx** out) {
   kst_ctx* c = new (std::nothrow) kst_ctx();
   if (!c) return KST_ERR_CUDA;
   c->device = device;
-  // K1 engine default: int8 tensor-core slices (6 x 7 bits: S relative error
-  // ~1e-11, see gram_ozaki.cu) when cuBLAS is loadable, else FP64 DMMA.
-  // Override: KST_GRAM=int8|dmma, KST_GRAM_SLICES=3..8.
-  c->gram_slices = 6;
-  c->gram_mode = kst::ozaki_available() ? 1 : 0;
+  // K1 engine default: the CRT int8 Gram on the hand-written tcgen05 kernel
+  // with 10 moduli (x rounded to >= 32 bits; measured at full size: spatial
+  // factor 5e-13, projectors 1e-13, residuals at their 1e-10 floor, see
+  // gram_crt.cu / DESIGN.md); else int8 slices (6) with cuBLAS; else FP64 DMMA.
+  // Override: KST_GRAM=crt|crt-cublas|int8|dmma, KST_GRAM_SLICES (moduli or slices).
+  const bool i8 = kst::ozaki_available(), tc = kst::crt_tc_available();
+  c->gram_mode = tc ? 2 : i8 ? 1 : 0;
+  c->gram_slices = tc ? 10 : 6;
   if (const char* e = getenv("KST_GRAM")) {
-    const bool i8 = kst::ozaki_available();
-    c->gram_mode = (strcmp(e, "int8") == 0 && i8)                               ? 1
-                   : (strcmp(e, "crt") == 0 && kst::crt_tc_available())        ? 2
-                   : (strcmp(e, "crt-cublas") == 0 && i8)                      ? 3
-                                                                               : 0;
-    if (c->gram_mode >= 2) c->gram_slices = 10;
+    c->gram_mode = (strcmp(e, "int8") == 0 && i8)               ? 1
+                   : (strcmp(e, "crt") == 0 && tc)              ? 2
+                   : (strcmp(e, "crt-cublas") == 0 && i8)       ? 3
+                                                                : 0;
+    c->gram_slices = c->gram_mode >= 2 ? 10 : 6;
   }
   if (const char* e = getenv("KST_GRAM_SLICES"))
     c->gram_slices = c->gram_mode >= 2 ? std::min(14, std::max(8, atoi(e)))

@@ -59,7 +59,22 @@ __constant__ CrtConst c_crt;
 // element into its 2N residue bytes (smem [i][part][a][k]); phase 2 writes
 // every (a, i, part) row segment with 4-byte stores coalesced over k.
 constexpr int CR_A = 16, CR_K = 64, CR_KP = CR_K + 4;
-template <int NM>
+
+// (h 2^32 + mid 2^16 + lo - 2^48) mod m as an int8 in [-128, 127]; m is a
+// compile-time constant after unrolling, so "% m" is a multiply-high sequence.
+// UNSIGNED: the residue in [0, m) as a uint8 (tcgen05 kind::i8 with unsigned
+// operands); else centred into [-128, 127] (cuBLAS signed int8 GEMMs).
+template <bool UNSIGNED>
+__device__ __forceinline__ uint8_t crt_residue8(int m, uint32_t h, uint32_t mid, uint32_t lo) {
+  const uint32_t um = (uint32_t)m;
+  const uint32_t c16 = 65536u % um, c32 = (c16 * c16) % um, c48 = (c32 * c16) % um;
+  const uint32_t t = h * c32 + mid * c16 + lo + (um - c48);  // < 2^27, == x' mod m
+  const uint32_t r = t % um;                                   // [0, m)
+  if (UNSIGNED) return (uint8_t)r;
+  return (uint8_t)(int8_t)(r >= 128u ? (int)r - m : (int)r);  // |r| <= 128
+}
+
+template <int NM, bool UNSIGNED>
 __global__ void __launch_bounds__(256) crt_residue_kernel(
     const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d, int64_t dpad,
     const int* __restrict__ expo, int beta, int8_t* __restrict__ R) {
@@ -74,16 +89,22 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
     for (int r = tid / CR_A; r < CR_K; r += 256 / CR_A) {
       const int64_t k = k0 + r;
       const cplx v = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
-      const double xr = rint(v.x * sc), xi = rint(v.y * sc);  // exact, |.| <= 2^beta
-      sb[0][0][c][r] = (int8_t)(long long)xr;                  // mod 256: low byte
-      sb[0][1][c][r] = (int8_t)(long long)xi;
+      // x' = rint(x 2^(beta - E)), |x'| <= 2^48, read off the mantissa of
+      // x + 1.5 2^52 (round to nearest even, FP64 adder only), then biased by
+      // 2^48 and cut into 17 + 16 + 16 bits for 32-bit modular arithmetic
+      const long long magic = 0x4338000000000000ll;
+      const long long xr = __double_as_longlong(fma(v.x, sc, 6755399441055744.0)) - magic;
+      const long long xi = __double_as_longlong(fma(v.y, sc, 6755399441055744.0)) - magic;
+      const unsigned long long ur = (unsigned long long)(xr + (1ll << 48));
+      const unsigned long long ui = (unsigned long long)(xi + (1ll << 48));
+      const uint32_t hr = (uint32_t)(ur >> 32), mr = (uint32_t)(ur >> 16) & 0xFFFFu,
+                     lr = (uint32_t)ur & 0xFFFFu;
+      const uint32_t hi = (uint32_t)(ui >> 32), mi = (uint32_t)(ui >> 16) & 0xFFFFu,
+                     li = (uint32_t)ui & 0xFFFFu;
 #pragma unroll
-      for (int i = 1; i < NM; ++i) {
-        // |x'| <= 2^48 keeps x' / m within 1/(16 m) of its double product, so
-        // rint picks the exact nearest quotient and the residue is centred
-        const double md = (double)modulus(i), inv = 1.0 / (double)modulus(i);
-        sb[i][0][c][r] = (int8_t)(int)fma(-md, rint(xr * inv), xr);
-        sb[i][1][c][r] = (int8_t)(int)fma(-md, rint(xi * inv), xi);
+      for (int i = 0; i < NM; ++i) {
+        sb[i][0][c][r] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hr, mr, lr);
+        sb[i][1][c][r] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hi, mi, li);
       }
     }
   }
@@ -111,6 +132,17 @@ __device__ __forceinline__ double crt_finish(double s0, double s1, double s2, fl
   return fma(t, 549755813888.0, s2);
 }
 
+// v 2^sh / n: exact power-of-two scaling (exponent splice while 2^sh is a
+// normal double), then the quotient by one Newton correction of v (1/n)
+// (within an ulp of the correctly rounded v / n; no FP64 divide per entry)
+__device__ __forceinline__ double crt_scale(double v, int sh, double dn, double rn) {
+  const double x = (sh >= -1022 && sh <= 1023)
+                       ? v * __longlong_as_double((long long)(sh + 1023) << 52)
+                       : ldexp(v, sh);
+  const double q = x * rn;
+  return fma(fma(-q, dn, x), rn, q);
+}
+
 // S from the per-modulus int32 products (column-major, ld = dpad): CTA per
 // (bi <= bj) pair of 32x32 tiles, writes S[a][b] and S[b][a] = conj.
 template <int NM>
@@ -119,6 +151,7 @@ __global__ void __launch_bounds__(256, 2) crt_combine_kernel(
     const int* __restrict__ expo, int beta, double dn, int T, cplx* __restrict__ S) {
   __shared__ uint8_t mt[NM][32][33];  // mt[i][j][l] = M_i[b0+j][a0+l] mod m_i
   __shared__ cplx vt[32][33];         // vt[j][l] = S[a0+j][b0+l]
+  const double rn = 1.0 / dn;
   const int t = blockIdx.x;
   double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * t;
   int bi = (int)floor(((2.0 * T + 1.0) - sqrt(disc)) * 0.5);
@@ -192,7 +225,7 @@ __global__ void __launch_bounds__(256, 2) crt_combine_kernel(
         const double vre = crt_finish(re0[c], re1[c], re2[c], rek[c]);
         const double vim = crt_finish(im0[c], im1[c], im2[c], imk[c]);
         const int sh = ea + eb - 2 * beta;
-        v = cmk(ldexp(vre, sh) / dn, ldexp(vim, sh) / dn);
+        v = cmk(crt_scale(vre, sh, dn, rn), crt_scale(vim, sh, dn, rn));
       }
       vt[q4 + c][r] = v;
     }
@@ -274,9 +307,12 @@ const HostCrt& host_crt(int nmod) {
 
 template <int NM>
 void launch_crt(const cplx* X, int64_t n, int64_t npad, int64_t d, int64_t dpad, const int* expo,
-                int beta, int8_t* R, cudaStream_t st) {
-  crt_residue_kernel<NM><<<dim3(cdiv(dpad, CR_A), cdiv(npad, CR_K)), 256, 0, st>>>(
-      X, n, npad, d, dpad, expo, beta, R);
+                int beta, int8_t* R, bool uns, cudaStream_t st) {
+  const dim3 grid(cdiv(dpad, CR_A), cdiv(npad, CR_K));
+  if (uns)
+    crt_residue_kernel<NM, true><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
+  else
+    crt_residue_kernel<NM, false><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
 }
 template <int NM>
 void launch_combine(const int32_t* GRe, const int32_t* GM, int64_t dpad, int64_t d, const int* expo,
@@ -319,10 +355,12 @@ constexpr int TC_THREADS = 576;            // 2 control warps + 16 epilogue warp
 constexpr int TC_EPI_THREADS = 512;
 constexpr int TC_TMEM_COLS = 512;            // Re | M | MT (3 x 128), power-of-2 allocation
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_BYTES + 1024 + 256;
-// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A/B signed int8
-// (bits 7-9, 10-12 = 1), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
-constexpr uint32_t kTcIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                              ((uint32_t)(TC_BM >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A/B unsigned 8-bit
+// (bits 7-9, 10-12 = 0; residues in [0, m)), both K-major, N >> 3 at bit 17,
+// M >> 4 at bit 24. Products < 2^16, so |Re| < 2n 2^16 and |M|, |MT| < n 2^16.
+constexpr uint32_t kTcIdesc = (2u << 4) | ((uint32_t)(TC_BM >> 3) << 17) |
+                              ((uint32_t)(TC_BM >> 4) << 24);
+constexpr int64_t kTcMaxN = 8192;  // keeps every accumulator inside tc_mod's range
 
 __constant__ int c_tc_mod[kMaxMod];
 __constant__ uint32_t c_tc_magic[kMaxMod];  // ceil(2^39 / m), 2^31 for m = 256
@@ -417,18 +455,22 @@ __host__ __device__ __forceinline__ void upper_tile(int t, int T, int& I, int& J
   J = i + (t - (i * T - i * (i - 1) / 2));
 }
 
-// v mod m in [0, m) for |v| < 2^27, integer pipes only (no conversions):
-// u = v + m 2^20 in [0, 2^29), q = floor(u / m) = umulhi(u, ceil(2^39 / m)) >> 7,
-// exact for u < 2^29 and 128 < m <= 256 (magic = 2^31 for m = 256).
+// v mod m in [0, m), integer pipes only (no conversions): u = v + m 2^22,
+// q = floor(u / m) = umulhi(u, ceil(2^39 / m)) >> 7, exact for u < 2^31 and
+// 128 < m <= 256 (magic = 2^31 for m = 256). n <= kTcMaxN keeps
+// -m 2^22 < v < 2^31 - m 2^22 for every Re / Im accumulator.
 __device__ __forceinline__ uint32_t tc_mod(int v, int m, uint32_t magic) {
-  const uint32_t u = (uint32_t)(v + (m << 20));
+  const uint32_t u = (uint32_t)(v + (m << 22));
   return u - (uint32_t)m * (__umulhi(u, magic) >> 7);
 }
 
 // res[t][i][comp][row][col] (uint8; comp 0 = Re, 1 = Im), t = upper tile index
 __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
     const __grid_constant__ CUtensorMap tmap, int T, int ntiles, int nmod, int nkb,
-    uint8_t* __restrict__ res) {
+    uint8_t* __restrict__ res, unsigned long long* __restrict__ prof) {
+  // prof (debug, KST_TC_PROF=1): cycles the producer waits for free slots, the
+  // MMA thread waits for data / for TMEM, and the MMA thread's total span
+  long long w_empty = 0, w_full = 0, w_tmem = 0, t_begin = clock64();
   extern __shared__ uint8_t tc_smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(base + TC_STAGES * TC_STAGE_BYTES);
@@ -469,7 +511,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             const int s = it % TC_STAGES;
             const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-            mbar_wait(&empty[s], ph ^ 1u);
+            if (prof) {
+              const long long c0 = clock64();
+              mbar_wait(&empty[s], ph ^ 1u);
+              w_empty += clock64() - c0;
+            } else {
+              mbar_wait(&empty[s], ph ^ 1u);
+            }
             uint8_t* st = base + s * TC_STAGE_BYTES;
             mbar_expect_tx(&full[s], TC_STAGE_BYTES);
             tma_load3(&tmap, &full[s], st, kb * TC_BK, 2 * i, I * TC_BM);
@@ -478,18 +526,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
             tma_load3(&tmap, &full[s], st + 3 * TC_OPER, kb * TC_BK, 2 * i + 1, J * TC_BM);
           }
       }
+      if (prof) atomicAdd(&prof[0], (unsigned long long)w_empty);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       int it = 0, pass = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
         for (int i = 0; i < nmod; ++i, ++pass) {
-          mbar_wait(tempty, ((uint32_t)pass & 1u) ^ 1u);  // epilogue drained TMEM
+          {
+            const long long c0 = prof ? clock64() : 0;
+            mbar_wait(tempty, ((uint32_t)pass & 1u) ^ 1u);  // epilogue drained TMEM
+            if (prof) w_tmem += clock64() - c0;
+          }
           tc_fence_after();
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             const int s = it % TC_STAGES;
             const uint32_t ph = (uint32_t)(it / TC_STAGES) & 1u;
-            mbar_wait(&full[s], ph);
+            {
+              const long long c0 = prof ? clock64() : 0;
+              mbar_wait(&full[s], ph);
+              if (prof) w_full += clock64() - c0;
+            }
             tc_fence_after();
             const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
 #pragma unroll
@@ -508,6 +565,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
           }
           tc_commit(tfull);  // accumulators of modulus i complete
         }
+      if (prof) {
+        atomicAdd(&prof[1], (unsigned long long)w_full);
+        atomicAdd(&prof[2], (unsigned long long)w_tmem);
+        atomicAdd(&prof[3], (unsigned long long)(clock64() - t_begin));
+      }
     }
   } else {  // ---------------- epilogue: TMEM -> residues
     // 16 warps: lane quarter q = warp % 4 (TMEM lanes 32q..32q+31 = tile rows),
@@ -572,6 +634,7 @@ __global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
     const uint8_t* __restrict__ res, int T, const int* __restrict__ expo, int beta, double dn,
     int64_t d, cplx* __restrict__ S) {
   __shared__ cplx vt[32][33];
+  const double rn = 1.0 / dn;
   const int t = blockIdx.x >> 4, sb = blockIdx.x & 15;
   int I, J;
   upper_tile(t, T, I, J);
@@ -629,7 +692,7 @@ __global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
       const double vre = crt_finish(re0[c], re1[c], re2[c], rek[c]);
       const double vim = crt_finish(im0[c], im1[c], im2[c], imk[c]);
       const int sh = ea + eb - 2 * beta;
-      v = cmk(ldexp(vre, sh) / dn, ldexp(vim, sh) / dn);
+      v = cmk(crt_scale(vre, sh, dn, rn), crt_scale(vim, sh, dn, rn));
     }
     vt[r][q4 + c] = v;
   }
@@ -751,15 +814,32 @@ static int scm_crt_tc(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S
   }
   i8::colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
   KST_LAUNCH(ctx);
-  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, st)));
+  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, true, st)));
   KST_LAUNCH(ctx);
   KST_CUDA(ctx, cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)TC_SMEM));
   stage_mark(ctx, 5, st);  // profiling: int8 tensor-core span (events 5..6)
-  gram_tc_kernel<<<(unsigned)std::min(ntiles, nsm), TC_THREADS, TC_SMEM, st>>>(map, T, ntiles, nmod,
-                                                                              nkb, res);
+  static const bool prof_on = getenv("KST_TC_PROF") && atoi(getenv("KST_TC_PROF")) != 0;
+  unsigned long long* prof = nullptr;
+  if (prof_on) {
+    prof = (unsigned long long*)ws_get(ctx, WS_TMP, 64);
+    if (!prof) return set_err(ctx, KST_ERR_CUDA, "scm_crt: profile buffer");
+    KST_CUDA(ctx, cudaMemsetAsync(prof, 0, 64, st));
+  }
+  const int grid = std::min(ntiles, nsm);
+  gram_tc_kernel<<<(unsigned)grid, TC_THREADS, TC_SMEM, st>>>(map, T, ntiles, nmod, nkb, res, prof);
   KST_LAUNCH(ctx);
   stage_mark(ctx, 6, st);
+  if (prof_on) {  // debug: where the pipeline waits (cycles summed over CTAs)
+    unsigned long long h[4];
+    KST_CUDA(ctx, cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    KST_CUDA(ctx, cudaStreamSynchronize(st));
+    fprintf(stderr,
+            "[gram_tc] per CTA (cycles): span %.0f, MMA waits data %.0f (%.1f%%), TMEM %.0f "
+            "(%.1f%%), producer waits slots %.0f\n",
+            (double)h[3] / grid, (double)h[1] / grid, 100.0 * h[1] / h[3], (double)h[2] / grid,
+            100.0 * h[2] / h[3], (double)h[0] / grid);
+  }
   ctx->last_int8_ops = 2.0 * 4.0 * (double)TC_BM * TC_BM * (double)nkb * TC_BK * nmod * ntiles;
   KST_CRT_DISPATCH(nmod, (launch_tile_combine<NM_>(res, T, ntiles, expo, beta, (double)n, d, S, st)));
   KST_LAUNCH(ctx);
@@ -777,7 +857,9 @@ int scm_crt(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod
     return set_err(ctx, KST_ERR_DIMENSION, "CRT Gram: int32 products need n <= 65536");
   const HostCrt& hc = host_crt(nmod);
   KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_crt, &hc.c, sizeof(CrtConst), 0, cudaMemcpyHostToDevice, st));
-  if (use_tc) return scm_crt_tc(ctx, X, n, d, S, nmod, beta, st);
+  // n > kTcMaxN (beyond every configuration here) takes the library-GEMM form
+  // of the same numerics
+  if (use_tc && n <= kTcMaxN) return scm_crt_tc(ctx, X, n, d, S, nmod, beta, st);
   if (!i8::load_blas()) return set_err(ctx, KST_ERR_CUDA, "scm_crt: cuBLAS not loadable");
   cublasHandle_t h = i8::blas_handle(ctx, st);
   if (!h) return set_err(ctx, KST_ERR_CUDA, "cublasCreate failed");
@@ -818,7 +900,7 @@ int scm_crt(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod
   }
   i8::colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
   KST_LAUNCH(ctx);
-  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, st)));
+  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, false, st)));
   KST_LAUNCH(ctx);
   stage_mark(ctx, 5, st);  // profiling: int8 GEMM span (events 5..6)
   const int32_t one = 1, zero = 0;

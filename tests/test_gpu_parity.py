@@ -26,6 +26,15 @@ import paper_1604_03622_b200 as kst  # noqa: E402
 from oracle import kron_oracle as orc  # noqa: E402
 
 
+MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
+
+
+def crt_beta(nmod, n):
+    """gram_crt.cu crt_beta: largest beta with 2n 2^(2 beta) <= P/4 (capped at 48)."""
+    log2p = sum(np.log2(MODULI[:nmod]))
+    return min(int(np.floor((log2p - 3 - np.log2(n) - 1e-6) / 2)), 48)
+
+
 def _proj(u):
     u = np.asarray(u)
     return u @ u.conj().T
@@ -45,9 +54,15 @@ def test_step_api_matches_reference(name):
         s = scm.matrix
         assert np.array_equal(s, s.conj().T)
         # FP64 DMMA engine: rounding only; int8-slice engine: slice truncation
-        # bound ~(slices+1) 2^(-7 slices) (gram_ozaki.cu)
+        # bound ~(slices+1) 2^(-7 slices) (gram_ozaki.cu); CRT engine: rounding
+        # x to beta bits, 64 2^-beta (gram_crt.cu)
         mode, slices = kst.lrkron.get_gram_engine()
-        tol = 1e-13 if mode == "dmma" else 64 * (slices + 1) * 2.0 ** (-7 * slices)
+        if mode == "dmma":
+            tol = 1e-13
+        elif mode == "int8":
+            tol = 64 * (slices + 1) * 2.0 ** (-7 * slices)
+        else:
+            tol = 64 * 2.0 ** (-crt_beta(slices, n))
         assert np.linalg.norm(s - d["scm"]) <= tol * np.linalg.norm(d["scm"])
     est = kst.lr_kron_estimate(scm, int(d["ra"]), int(d["rb"]), tol=float(d["tol"]),
                                max_iter=int(d["max_iter"]))
@@ -229,9 +244,6 @@ def test_int8_gram_engine_error_bound(slices):
     assert np.linalg.norm(s - ref) <= bound * np.linalg.norm(ref)
 
 
-MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
-
-
 @pytest.mark.parametrize("nmod", [8, 9, 10, 12, 14])
 def test_crt_gram_engine_error_bound(nmod):
     """The modular (CRT) int8 Gram against the FP64 DMMA Gram: exactly
@@ -250,8 +262,7 @@ def test_crt_gram_engine_error_bound(nmod):
         s = kst.sample_covariance(snaps, 3, 256).matrix
     finally:
         lrkron.set_gram_engine(*before)
-    log2p = sum(np.log2(MODULI[:nmod]))
-    beta = min(int(np.floor((log2p - 3 - np.log2(n) - 1e-6) / 2)), 48)
+    beta = crt_beta(nmod, n)
     assert np.array_equal(s, s.conj().T)
     assert not np.any(np.diagonal(s).imag)
     dg = np.sqrt(np.outer(ref.diagonal().real, ref.diagonal().real))

@@ -15,7 +15,8 @@ import numpy as np
 
 from .errors import CudaError, DataError, DegenerateInputError, DimensionError, KronStapError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libkst_b200.so")
+LIB_PATH = os.environ.get("KST_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "_lib", "libkst_b200.so")  # override: A/B builds
 
 _vp = C.c_void_p
 _i = C.c_int

@@ -10,13 +10,14 @@
 // and the exact integer Gram entries follow from
 //     V = sum_i c_i w_i - k P,   w_i = (P/m_i) ((P/m_i)^-1 mod m_i) < P,
 //     c_i = Re_i mod m_i    (Im: c_i = (M_i[a,b] - M_i[b,a]) mod m_i),
-//     k = round(sum_i c_i w_i / P) = round(sum_i c_i y_i / m_i)   (FP32 suffices).
+//     k = round(sum_i c_i w_i / P)   (from the top chunk alone, see crt_finish).
 // beta is the largest value with 2n 2^(2 beta) <= P/4, so |V| <= P/4 and V is
-// the exact integer product; w_i and P are cut into 39-bit chunks so every
-// chunk sum is exact in FP64 and V costs two roundings. The only error is
-// rounding x to beta bits: ~n 2^-beta of max|x_a| max|x_b| (13 moduli,
-// n = 2001: beta = 44, vs 42 kept bits for 6 slices). N moduli cost 3N units
-// of int8 GEMM depth-n work against 3 s(s+1)/2 for s slices (13 vs 21 at s = 6).
+// the exact integer product; w_i and P are cut into 40-bit (<= 10 moduli) or
+// 39-bit chunks so every chunk sum is exact in FP64 and V costs one or two
+// roundings. The only error is rounding x to beta bits: ~n 2^-beta of
+// max|x_a| max|x_b| (10 moduli, n = 2001: beta = 32; rounding, unlike slice
+// truncation, is unbiased). N moduli cost 3N units of int8 GEMM depth-n work
+// against 3 s(s+1)/2 for s slices (10 vs 21 at s = 6).
 //
 // S is exactly Hermitian with a real diagonal (Im V[a,a] = 0 by construction);
 // non-finite columns poison their S entries with NaN (DataError upstream).
@@ -45,10 +46,14 @@ __host__ __device__ constexpr int modulus(int i) {
        : i == 12 ? 211 : i == 13 ? 199 : i == 14 ? 197 : 193;
 }
 
+// CRT weights cut into NCH chunks of CB bits: NCH = 2, CB = 40 while P < 2^80
+// (<= 10 moduli), else NCH = 3, CB = 39 (P < 2^117).
+__host__ __device__ constexpr int crt_nch(int nmod) { return nmod <= 10 ? 2 : 3; }
+__host__ __device__ constexpr int crt_cb(int nmod) { return nmod <= 10 ? 40 : 39; }
 struct CrtConst {
-  double w[kMaxMod][3];  // w_i = (w0 2^39 + w1) 2^39 + w2, chunks < 2^39
+  double w[kMaxMod][3];  // w_i chunks, most significant first
   double p[3];           // P, same chunks
-  float ym[kMaxMod];     // y_i / m_i
+  double kscale;         // 2^CB / P: quotient estimate from the upper chunks
 };
 __constant__ CrtConst c_crt;
 
@@ -58,7 +63,10 @@ __constant__ CrtConst c_crt;
 // CTA = 16 columns x 64 rows; phase 1 reads X coalesced over a and cuts each
 // element into its 2N residue bytes (smem [i][part][a][k]); phase 2 writes
 // every (a, i, part) row segment with 4-byte stores coalesced over k.
-constexpr int CR_A = 16, CR_K = 64, CR_KP = CR_K + 4;
+#ifndef KST_CR_SUB
+#define KST_CR_SUB 1
+#endif
+constexpr int CR_A = 16, CR_K = 64, CR_KP = CR_K + 4, CR_SUB = KST_CR_SUB;
 
 // (h 2^32 + mid 2^16 + lo - 2^48) mod m as an int8 in [-128, 127]; m is a
 // compile-time constant after unrolling, so "% m" is a multiply-high sequence.
@@ -79,22 +87,40 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
     const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d, int64_t dpad,
     const int* __restrict__ expo, int beta, int8_t* __restrict__ R) {
   __shared__ __align__(16) int8_t sb[NM][2][CR_A][CR_KP];
-  const int64_t k0 = (int64_t)blockIdx.y * CR_K, a0 = (int64_t)blockIdx.x * CR_A;
+  const int64_t a0 = (int64_t)blockIdx.x * CR_A;
   const int tid = threadIdx.x;
-  {
-    const int c = tid & (CR_A - 1);
-    const int64_t a = a0 + c;
-    const int e = a < d ? expo[a] : 0;
-    const double sc = (e == kNaNExpo) ? 0.0 : ldexp(1.0, beta - e);
-    for (int r = tid / CR_A; r < CR_K; r += 256 / CR_A) {
-      const int64_t k = k0 + r;
-      const cplx v = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+  const int c = tid & (CR_A - 1), r_first = tid / CR_A;
+  constexpr int RPT = CR_K / (256 / CR_A);  // rows per thread per sub-block (4)
+  const int64_t a = a0 + c;
+  const int e = a < d ? expo[a] : 0;
+  // 2^(beta - E) as two spliced factors (each a normal double); 0 for NaN columns
+  const int sh = max(-2044, min(2046, beta - e)), h1 = sh / 2, h2 = sh - h1;
+  const double s1 = (e == kNaNExpo) ? 0.0 : __longlong_as_double((long long)(h1 + 1023) << 52);
+  const double s2 = __longlong_as_double((long long)(h2 + 1023) << 52);
+  const int lw = tid & 15;
+  // CR_SUB consecutive 64-row sub-blocks per CTA; the next sub-block's X
+  // values are loaded while the current one is cut and written
+  cplx v[RPT];
+  int64_t kb0 = (int64_t)blockIdx.y * CR_K * CR_SUB;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int64_t k = kb0 + r_first + j * (256 / CR_A);
+    v[j] = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+  }
+#pragma unroll 1
+  for (int sub = 0; sub < CR_SUB; ++sub, kb0 += CR_K) {
+    if (kb0 >= npad) break;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const int r = r_first + j * (256 / CR_A);
       // x' = rint(x 2^(beta - E)), |x'| <= 2^48, read off the mantissa of
       // x + 1.5 2^52 (round to nearest even, FP64 adder only), then biased by
       // 2^48 and cut into 17 + 16 + 16 bits for 32-bit modular arithmetic
       const long long magic = 0x4338000000000000ll;
-      const long long xr = __double_as_longlong(fma(v.x, sc, 6755399441055744.0)) - magic;
-      const long long xi = __double_as_longlong(fma(v.y, sc, 6755399441055744.0)) - magic;
+      const long long xr =
+          __double_as_longlong(fma(v[j].x * s1, s2, 6755399441055744.0)) - magic;
+      const long long xi =
+          __double_as_longlong(fma(v[j].y * s1, s2, 6755399441055744.0)) - magic;
       const unsigned long long ur = (unsigned long long)(xr + (1ll << 48));
       const unsigned long long ui = (unsigned long long)(xi + (1ll << 48));
       const uint32_t hr = (uint32_t)(ur >> 32), mr = (uint32_t)(ur >> 16) & 0xFFFFu,
@@ -107,38 +133,61 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
         sb[i][1][c][r] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hi, mi, li);
       }
     }
-  }
-  __syncthreads();
-  const int lw = tid & 15;
-  const int64_t k = k0 + 4 * lw;
-  if (k >= npad) return;  // npad is a multiple of 16: whole words only
-  for (int seg = tid >> 4; seg < CR_A * NM * 2; seg += 16) {
-    const int cc = seg / (2 * NM), rem = seg % (2 * NM), i = rem >> 1, part = rem & 1;
-    const int64_t a = a0 + cc;
-    if (a >= dpad) continue;
-    *(uint32_t*)(R + (((size_t)a * NM + i) * 2 + part) * npad + k) =
-        *(const uint32_t*)&sb[i][part][cc][4 * lw];
+    if (sub + 1 < CR_SUB) {  // prefetch the next sub-block
+#pragma unroll
+      for (int j = 0; j < RPT; ++j) {
+        const int64_t k = kb0 + CR_K + r_first + j * (256 / CR_A);
+        v[j] = (k < n && a < d) ? X[k * d + a] : cmk(0, 0);
+      }
+    }
+    __syncthreads();
+    const int64_t k = kb0 + 4 * lw;
+    if (k < npad) {  // npad is a multiple of 16: whole words only
+      for (int seg = tid >> 4; seg < CR_A * NM * 2; seg += 16) {
+        const int cc = seg / (2 * NM), rem = seg % (2 * NM), i = rem >> 1, part = rem & 1;
+        const int64_t aa = a0 + cc;
+        if (aa >= dpad) continue;
+        *(uint32_t*)(R + (((size_t)aa * NM + i) * 2 + part) * npad + k) =
+            *(const uint32_t*)&sb[i][part][cc][4 * lw];
+      }
+    }
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------- reconstruction
-// chunk sums (s0, s1, s2) and the FP32 quotient estimate -> V (two roundings)
-__device__ __forceinline__ double crt_finish(double s0, double s1, double s2, float kf) {
-  const double k = (double)rintf(kf);
-  s0 = fma(-k, c_crt.p[0], s0);  // exact: |k P_j| < 2^51, |result| < 2^52
+// chunk sums s_j = sum_i c_i w_ij (exact) -> V = sum_i c_i w_i - k P with
+// k = round(sum_i c_i w_i / P) estimated from all but the lowest chunk:
+// (s_0 [2^CB + s_1]) 2^CB / P; the dropped chunk moves the quotient by
+// < nmod 2^9 2^CB / P < 1e-8, far inside the |V| <= P/4 margin. |k| < 2 nmod,
+// so every s_j - k P_j is exact; V costs NCH - 1 roundings.
+template <int NCH>
+__device__ __forceinline__ double crt_finish(double s0, double s1, double s2) {
+  const double est = (NCH == 2) ? s0 : fma(s0, 549755813888.0, s1);
+  const double k = rint(est * c_crt.kscale);
+  s0 = fma(-k, c_crt.p[0], s0);
   s1 = fma(-k, c_crt.p[1], s1);
+  if (NCH == 2) return fma(s0, 1099511627776.0, s1);  // 2^40
   s2 = fma(-k, c_crt.p[2], s2);
   const double t = fma(s0, 549755813888.0, s1);  // 2^39
   return fma(t, 549755813888.0, s2);
 }
 
-// v 2^sh / n: exact power-of-two scaling (exponent splice while 2^sh is a
-// normal double), then the quotient by one Newton correction of v (1/n)
-// (within an ulp of the correctly rounded v / n; no FP64 divide per entry)
+// v 2^sh / n: exact power-of-two scaling as two multiplications by spliced
+// powers 2^(sh/2), 2^(sh - sh/2) (each a normal double for |sh| <= 2044), then
+// the quotient by one Newton correction of v (1/n) (within an ulp of the
+// correctly rounded v / n; no FP64 divide or ldexp per entry)
 __device__ __forceinline__ double crt_scale(double v, int sh, double dn, double rn) {
+#ifdef KST_SCALE_SPLIT
+  sh = max(-2044, min(2046, sh));
+  const int h1 = sh >> 1, h2 = sh - h1;
+  const double x = v * __longlong_as_double((long long)(h1 + 1023) << 52) *
+                   __longlong_as_double((long long)(h2 + 1023) << 52);
+#else  // measured faster (A/B, tools/ab_kernels.sh)
   const double x = (sh >= -1022 && sh <= 1023)
                        ? v * __longlong_as_double((long long)(sh + 1023) << 52)
                        : ldexp(v, sh);
+#endif
   const double q = x * rn;
   return fma(fma(-q, dn, x), rn, q);
 }
@@ -182,13 +231,10 @@ __global__ void __launch_bounds__(256, 2) crt_combine_kernel(
   {
     const int64_t b = b0 + r;
     const size_t idx = (size_t)(a0 + q4) + (size_t)b * dpad;
+    constexpr int NCH = crt_nch(NM);
     double re0[4], re1[4], re2[4], im0[4], im1[4], im2[4];
-    float rek[4], imk[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
-      rek[c] = imk[c] = 0.0f;
-    }
+    for (int c = 0; c < 4; ++c) re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
 #pragma unroll
     for (int i = 0; i < NM; ++i) {
       const int m = modulus(i);
@@ -196,7 +242,6 @@ __global__ void __launch_bounds__(256, 2) crt_combine_kernel(
       const int4 vm = *(const int4*)(GM + (size_t)i * plane + idx);
       const int ur[4] = {vr.x, vr.y, vr.z, vr.w}, um[4] = {vm.x, vm.y, vm.z, vm.w};
       const double w0 = c_crt.w[i][0], w1 = c_crt.w[i][1], w2 = c_crt.w[i][2];
-      const float ym = c_crt.ym[i];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int cre = ur[c] % m;  // (-m, m)
@@ -205,12 +250,12 @@ __global__ void __launch_bounds__(256, 2) crt_combine_kernel(
         const double dre = (double)cre, dim = (double)cim;
         re0[c] = fma(dre, w0, re0[c]);
         re1[c] = fma(dre, w1, re1[c]);
-        re2[c] = fma(dre, w2, re2[c]);
         im0[c] = fma(dim, w0, im0[c]);
         im1[c] = fma(dim, w1, im1[c]);
-        im2[c] = fma(dim, w2, im2[c]);
-        rek[c] = fmaf((float)cre, ym, rek[c]);
-        imk[c] = fmaf((float)cim, ym, imk[c]);
+        if (NCH == 3) {
+          re2[c] = fma(dre, w2, re2[c]);
+          im2[c] = fma(dim, w2, im2[c]);
+        }
       }
     }
     const int eb = (b < d) ? expo[b] : 0;
@@ -222,8 +267,8 @@ __global__ void __launch_bounds__(256, 2) crt_combine_kernel(
       if (ea == kNaNExpo || eb == kNaNExpo) {
         v = cmk(NAN, NAN);
       } else {
-        const double vre = crt_finish(re0[c], re1[c], re2[c], rek[c]);
-        const double vim = crt_finish(im0[c], im1[c], im2[c], imk[c]);
+        const double vre = crt_finish<NCH>(re0[c], re1[c], re2[c]);
+        const double vim = crt_finish<NCH>(im0[c], im1[c], im2[c]);
         const int sh = ea + eb - 2 * beta;
         v = cmk(crt_scale(vre, sh, dn, rn), crt_scale(vim, sh, dn, rn));
       }
@@ -281,11 +326,14 @@ const HostCrt& host_crt(int nmod) {
     P *= (u128)kModuli[i];
     lp += std::log2((double)kModuli[i]);
   }
-  const u128 mask = ((u128)1 << 39) - 1;
-  auto chunks = [&](u128 v, double* out) {
-    out[0] = (double)(unsigned long long)(v >> 78);
-    out[1] = (double)(unsigned long long)((v >> 39) & mask);
-    out[2] = (double)(unsigned long long)(v & mask);
+  const int nch = crt_nch(nmod), cb = crt_cb(nmod);
+  const u128 mask = ((u128)1 << cb) - 1;
+  auto chunks = [&](u128 v, double* out) {  // most significant chunk first
+    out[2] = 0.0;
+    for (int j = nch - 1; j >= 0; --j) {
+      out[j] = (double)(unsigned long long)(j == 0 ? v : (v & mask));
+      v >>= cb;
+    }
   };
   for (int i = 0; i < kMaxMod; ++i) {
     if (i < nmod) {
@@ -293,13 +341,12 @@ const HostCrt& host_crt(int nmod) {
       const u128 Q = P / (u128)m;
       const int y = modinv((int)(Q % (u128)m), m);
       chunks(Q * (u128)y, h.c.w[i]);
-      h.c.ym[i] = (float)((double)y / (double)m);
     } else {
       h.c.w[i][0] = h.c.w[i][1] = h.c.w[i][2] = 0.0;
-      h.c.ym[i] = 0.0f;
     }
   }
   chunks(P, h.c.p);
+  h.c.kscale = std::ldexp(1.0, cb) / (double)P;  // units of the estimate: 2^CB
   h.log2p = lp;
   h.nmod = nmod;
   return h;
@@ -308,7 +355,7 @@ const HostCrt& host_crt(int nmod) {
 template <int NM>
 void launch_crt(const cplx* X, int64_t n, int64_t npad, int64_t d, int64_t dpad, const int* expo,
                 int beta, int8_t* R, bool uns, cudaStream_t st) {
-  const dim3 grid(cdiv(dpad, CR_A), cdiv(npad, CR_K));
+  const dim3 grid(cdiv(dpad, CR_A), cdiv(npad, CR_K * CR_SUB));
   if (uns)
     crt_residue_kernel<NM, true><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
   else
@@ -643,13 +690,10 @@ __global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
   const int q4 = 4 * (tid & 7), r = tid >> 3;
   const int lr = 32 * sr + r, lc = 32 * sc + q4;  // tile-local row / first column
   const int64_t a = (int64_t)I * TC_BM + lr;
+  constexpr int NCH = crt_nch(NM);
   double re0[4], re1[4], re2[4], im0[4], im1[4], im2[4];
-  float rek[4], imk[4];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
-    rek[c] = imk[c] = 0.0f;
-  }
+  for (int c = 0; c < 4; ++c) re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
   const uint8_t* src = res + (size_t)t * NM * 2 * (TC_BM * TC_BM) + (size_t)lr * TC_BM + lc;
   uint32_t pr[NM], pm[NM];
 #pragma unroll
@@ -660,24 +704,21 @@ __global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const double w0 = c_crt.w[i][0], w1 = c_crt.w[i][1], w2 = c_crt.w[i][2];
-    const float ym = c_crt.ym[i];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const uint32_t cr = (pr[i] >> (8 * c)) & 0xFFu, cm = (pm[i] >> (8 * c)) & 0xFFu;
-      // byte -> double / float by exponent splicing (FP64 / FP32 pipes, not the
-      // conversion unit): 2^52 + c - 2^52, 2^23 + c - 2^23
+      // byte -> double by exponent splicing (FP64 adder, not the conversion
+      // unit): (2^52 + c) - 2^52
+      const uint32_t cr = __byte_perm(pr[i], 0, 0x4440 + c), cm = __byte_perm(pm[i], 0, 0x4440 + c);
       const double dr = __longlong_as_double(0x4330000000000000ll | cr) - 4503599627370496.0;
       const double dm = __longlong_as_double(0x4330000000000000ll | cm) - 4503599627370496.0;
-      const float fr = __int_as_float(0x4B000000 | (int)cr) - 8388608.0f;
-      const float fm = __int_as_float(0x4B000000 | (int)cm) - 8388608.0f;
       re0[c] = fma(dr, w0, re0[c]);
       re1[c] = fma(dr, w1, re1[c]);
-      re2[c] = fma(dr, w2, re2[c]);
       im0[c] = fma(dm, w0, im0[c]);
       im1[c] = fma(dm, w1, im1[c]);
-      im2[c] = fma(dm, w2, im2[c]);
-      rek[c] = fmaf(fr, ym, rek[c]);
-      imk[c] = fmaf(fm, ym, imk[c]);
+      if (NCH == 3) {
+        re2[c] = fma(dr, w2, re2[c]);
+        im2[c] = fma(dm, w2, im2[c]);
+      }
     }
   }
   const int ea = (a < d) ? expo[a] : 0;
@@ -689,8 +730,8 @@ __global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
     if (ea == kNaNExpo || eb == kNaNExpo) {
       v = cmk(NAN, NAN);
     } else {
-      const double vre = crt_finish(re0[c], re1[c], re2[c], rek[c]);
-      const double vim = crt_finish(im0[c], im1[c], im2[c], imk[c]);
+      const double vre = crt_finish<NCH>(re0[c], re1[c], re2[c]);
+      const double vim = crt_finish<NCH>(im0[c], im1[c], im2[c]);
       const int sh = ea + eb - 2 * beta;
       v = cmk(crt_scale(vre, sh, dn, rn), crt_scale(vim, sh, dn, rn));
     }

@@ -607,29 +607,52 @@ __device__ __forceinline__ void mgram_split_group(const cplx* __restrict__ S, in
   for (int k = 0; k < 2 * NK; ++k) m[k] = 0.0;
   const int nct = (q + MS_NTG - 1) / MS_NTG;
   const int ntile = rows * nct;
-  // every thread of the CTA issues its share of a tile; empty groups keep counts aligned
-  auto issue = [&](int t) {
-    if (t < ntile) {
-      const int r = r0 + t / nct, c0 = (t % nct) * MS_NTG;
-      cplx* buf = ring + (size_t)(t % MS_STAGES) * U * MS_NTG;
-      for (int e = threadIdx.x; e < U * MS_NTG; e += NG * MS_NTG) {
-        const int u = e / MS_NTG, pp = e % MS_NTG, c = c0 + pp;
-        if (c < q)
-          cp_async16(buf + e, S + ((int64_t)(u / P) * q + r) * d + (int64_t)(u % P) * q + c);
-      }
+  // every thread of the CTA issues its share of each tile: KPT fixed (u, pp)
+  // slots whose global offsets are computed once (no index division per tile)
+  constexpr int KPT = (U + NG - 1) / NG;
+  int64_t goff[KPT];
+  int eoff[KPT];
+#pragma unroll
+  for (int k = 0; k < KPT; ++k) {
+    const int e = threadIdx.x + k * NG * MS_NTG;
+    eoff[k] = e < U * MS_NTG ? e : -1;
+    const int u = e / MS_NTG, pp = e % MS_NTG;
+    goff[k] = (int64_t)(u / P) * q * d + (int64_t)(u % P) * q + pp;
+  }
+  int is_r = r0, is_c = 0, is_s = 0, is_t = 0;  // next tile to issue: row, col tile, stage
+  auto issue = [&]() {
+    if (is_t < ntile) {
+      cplx* buf = ring + (size_t)is_s * U * MS_NTG;
+      const cplx* src = S + (int64_t)is_r * d + is_c * MS_NTG;
+#pragma unroll
+      for (int k = 0; k < KPT; ++k)
+        if (eoff[k] >= 0 && is_c * MS_NTG + (eoff[k] % MS_NTG) < q)
+          cp_async16(buf + eoff[k], src + goff[k]);
     }
     cp_async_commit();
+    ++is_t;
+    is_s = (is_s + 1 == MS_STAGES) ? 0 : is_s + 1;
+    if (++is_c == nct) {
+      is_c = 0;
+      ++is_r;
+    }
   };
 #pragma unroll 1
-  for (int t = 0; t < MS_STAGES - 1; ++t) issue(t);
+  for (int t = 0; t < MS_STAGES - 1; ++t) issue();
+  int cr = r0, ccol = 0, cs = 0;  // tile being consumed
 #pragma unroll 1
   for (int t = 0; t < ntile; ++t) {
     cp_async_wait<MS_STAGES - 2>();
     __syncthreads();  // tile t visible to all; buffer of tile t-1 free
-    issue(t + MS_STAGES - 1);
-    const int r = r0 + t / nct, c = (t % nct) * MS_NTG + tg;
+    issue();
+    const int r = cr, c = ccol * MS_NTG + tg;
+    const cplx* buf = ring + (size_t)cs * U * MS_NTG + tg;
+    cs = (cs + 1 == MS_STAGES) ? 0 : cs + 1;
+    if (++ccol == nct) {
+      ccol = 0;
+      ++cr;
+    }
     if (c < q) {
-      const cplx* buf = ring + (size_t)(t % MS_STAGES) * U * MS_NTG + tg;
       cplx sv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) sv[u] = buf[u * MS_NTG];

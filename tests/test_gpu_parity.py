@@ -244,7 +244,7 @@ def test_int8_gram_engine_error_bound(slices):
     assert np.linalg.norm(s - ref) <= bound * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("nmod", [8, 9, 10, 12, 14])
+@pytest.mark.parametrize("nmod", [8, 9, 10, 11, 12, 13, 14])
 def test_crt_gram_engine_error_bound(nmod):
     """The modular (CRT) int8 Gram against the FP64 DMMA Gram: exactly
     Hermitian, real diagonal, error of rounding x to beta bits, where beta is

@@ -62,9 +62,13 @@ long long kst_launch_count(const kst_ctx* ctx);
 /* Sample-covariance engine (K1). mode 0: FP64 tensor-core DMMA tiles (FP64
  * rounding only). mode 1: int8 tensor-core GEMMs on exact 7-bit slices
  * (`slices` per operand, 3..8; relative error ~(slices+1) 2^-7*slices of
- * max|x_a| max|x_b| n). Default: mode 1 with 6 slices when cuBLAS is
- * loadable (else mode 0); env KST_GRAM=dmma|int8 and KST_GRAM_SLICES
- * override it at context creation. */
+ * max|x_a| max|x_b| n). mode 2: int8 residues modulo `slices` = 8..14
+ * coprime moduli recombined by the Chinese remainder theorem, products on the
+ * hand-written tcgen05 kernel (error: rounding x to beta bits, beta = 32 for
+ * 10 moduli and n = 2001). mode 3: mode 2's numerics on cuBLAS int8 GEMMs.
+ * Default: mode 2 with 10 moduli (else mode 1 with 6 slices, else mode 0);
+ * env KST_GRAM=dmma|int8|crt|crt-cublas and KST_GRAM_SLICES override it at
+ * context creation. */
 int kst_set_gram(kst_ctx* ctx, int mode, int slices);
 int kst_get_gram(const kst_ctx* ctx, int* mode, int* slices);
 /* int8 tensor ops issued by the last int8 Gram (0 if none); with profiling on,

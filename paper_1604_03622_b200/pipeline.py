@@ -54,10 +54,12 @@ def process_frame_device(cube, rank_spatial=1, rank_temporal=3, dopplers=None, s
 class FrameStream:
     """Host-buffer frame sequence with copy/compute overlap.
 
-    Frame i+1's host-to-device copy runs on a copy stream while frame i is
-    processed on the compute stream; each map is copied back on the copy
-    stream once its frame is done. With pinned host buffers the PCIe traffic
-    (192 MB in + 32 MB out per Gotcha frame) hides under the compute.
+    Frame i+1's host-to-device copy runs on an upload stream while frame i is
+    processed on the compute stream; each map is copied back on a separate
+    download stream once its frame is done, so the two PCIe directions (two
+    copy engines) overlap each other and the compute. With pinned host buffers
+    the traffic (192 MB in + 32 MB out per Gotcha frame) hides under the
+    compute up to the host-to-device bandwidth.
 
         fs = FrameStream(shape, device)
         for i, cube in enumerate(host_cubes):
@@ -76,7 +78,8 @@ class FrameStream:
         self.outs = [torch.empty((1, n, D), dtype=torch.float64, device=self.dev) for _ in range(2)]
         self.host_out = out_pinned if out_pinned is not None else [
             torch.empty((n, D), dtype=torch.float64).pin_memory() for _ in range(2)]
-        self.copy = torch.cuda.Stream(self.dev)
+        self.copy = torch.cuda.Stream(self.dev)       # host -> device
+        self.copy_back = torch.cuda.Stream(self.dev)  # device -> host
         self.comp = torch.cuda.current_stream(self.dev)
         self.ready = [torch.cuda.Event() for _ in range(2)]
         self.done = [torch.cuda.Event() for _ in range(2)]
@@ -108,12 +111,13 @@ class FrameStream:
             return None
         slot = self.pending
         self.comp.wait_event(self.ready[slot])
+        self.comp.wait_event(self.back[slot])  # map buffer read back (frame i - 2)
         process_frame_device(self.bufs[slot], *self.args, out=self.outs[slot], summary=self.summary)
         self.done[slot].record(self.comp)
-        with torch.cuda.stream(self.copy):
-            self.copy.wait_event(self.done[slot])
+        with torch.cuda.stream(self.copy_back):
+            self.copy_back.wait_event(self.done[slot])
             self.host_out[slot].copy_(self.outs[slot][0], non_blocking=True)
-            self.back[slot].record(self.copy)
+            self.back[slot].record(self.copy_back)
         self.pending = None
         return self.host_out[slot], self.back[slot]
 

@@ -276,19 +276,26 @@ __global__ void random_block_kernel(cplx* Z, int n, int s, uint64_t seed) {
 }
 
 // Z0 (n x s) = unit vectors e_i for the s largest Re(B_ii) (ties -> lower i).
-__global__ void unit_start_kernel(const cplx* __restrict__ B, int n, int s, cplx* __restrict__ Z) {
+// One CTA (1024 threads); the diagonal is gathered into smem once (all its
+// strided loads in flight together) when it fits (dyn_n > 0), and the s
+// selection rounds then read smem.
+__global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict__ B, int n, int s,
+                                                          cplx* __restrict__ Z, int dyn_n) {
+  extern __shared__ double dg[];
   __shared__ int picked[32];
-  __shared__ double bv[8];
-  __shared__ int bi[8];
+  __shared__ double bv[32];
+  __shared__ int bi[32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < dyn_n; i += blockDim.x) dg[i] = B[(size_t)i * n + i].x;
   for (int e = threadIdx.x; e < n * s; e += blockDim.x) Z[e] = cmk(0, 0);
+  __syncthreads();
   for (int k = 0; k < s; ++k) {
     double best = -INFINITY;
     int besti = n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       bool used = false;
       for (int j = 0; j < k; ++j) used |= picked[j] == i;
-      const double v = B[(size_t)i * n + i].x;
+      const double v = dyn_n ? dg[i] : B[(size_t)i * n + i].x;
       if (!used && (v > best || (v == best && i < besti))) {
         best = v;
         besti = i;
@@ -325,34 +332,57 @@ __global__ void unit_start_kernel(const cplx* __restrict__ B, int n, int s, cplx
 }
 
 // Final ordering (descending, reference tie rule) + pivot phase for the top r
-// Ritz vectors; single CTA of 256 threads, s <= 32.
-__global__ void finalize_top_kernel(const cplx* __restrict__ Z, int n, int s, int r,
-                                    const double* __restrict__ theta, double* __restrict__ vals_out,
-                                    cplx* __restrict__ vec_out) {
+// Ritz vectors; single CTA of 1024 threads, s <= 32. The pivot search (argmax
+// |Z[i][k]| per column, lowest index on ties) maps thread t to column t % s and
+// rows t / s, t / s + 1024 / s, ... (row-contiguous, coalesced loads), then
+// one warp per column reduces the row groups.
+__global__ void __launch_bounds__(1024) finalize_top_kernel(
+    const cplx* __restrict__ Z, int n, int s, int r, const double* __restrict__ theta,
+    double* __restrict__ vals_out, cplx* __restrict__ vec_out) {
   __shared__ int piv[32];
   __shared__ int order[32];
   __shared__ double phr[32], phi[32];
+  __shared__ double sbm[1024];
+  __shared__ int sbi[1024];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  for (int k = w; k < s; k += (int)(blockDim.x >> 5)) {
+  {
+    const int ng = (int)blockDim.x / s;  // row groups
+    const int k = threadIdx.x % s, g = threadIdx.x / s;
     double bm = -1.0;
-    int bi = 0;
-    for (int i = l; i < n; i += 32) {
-      const cplx v = Z[(size_t)i * s + k];
-      const double a = hypot(v.x, v.y);
-      if (a > bm) {
-        bm = a;
-        bi = i;
+    int bi = n;
+    if (g < ng)
+      for (int i = g; i < n; i += ng) {
+        const cplx v = Z[(size_t)i * s + k];
+        const double a = hypot(v.x, v.y);
+        if (a > bm) {
+          bm = a;
+          bi = i;
+        }
       }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, bm, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > bm || (ob == bm && oi < bi)) {
-        bm = ob;
-        bi = oi;
+    sbm[threadIdx.x] = bm;
+    sbi[threadIdx.x] = bi;
+    __syncthreads();
+    for (int kc = w; kc < s; kc += (int)(blockDim.x >> 5)) {
+      double b2 = -1.0;
+      int i2 = n;
+      for (int gg = l; gg < ng; gg += 32) {  // ascending groups: first maximum kept
+        const double ob = sbm[gg * s + kc];
+        const int oi = sbi[gg * s + kc];
+        if (ob > b2 || (ob == b2 && oi < i2)) {
+          b2 = ob;
+          i2 = oi;
+        }
       }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b2, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i2, o);
+        if (ob > b2 || (ob == b2 && oi < i2)) {
+          b2 = ob;
+          i2 = oi;
+        }
+      }
+      if (l == 0) piv[kc] = i2 < n ? i2 : 0;
     }
-    if (l == 0) piv[k] = bi;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -586,16 +616,21 @@ __global__ void __launch_bounds__(256) k4_small_kernel(const cplx* __restrict__ 
   }
   __syncthreads();
   // Fast path: scaled Cholesky QR. G~ = R^H R (R upper, in T), C = Q D R^-1.
-  // Taken when every pivot stays >= 1e-10 (well-conditioned block, i.e. all
-  // iterations after the first); otherwise fall through to SVQB by Jacobi.
+  // mode 0: taken when every pivot stays >= 1e-10 (well-conditioned block, all
+  // iterations after the warm-up), else SVQB by Jacobi. mode 1 (warm-up
+  // orthonormalisation, always followed by another pass): shifted Cholesky QR,
+  // G~ + 1e-11 I, never needs the Jacobi -- nearly dependent directions come
+  // out short instead of unit length and the next pass re-normalises them.
   {
     __shared__ int chol_ok;
-    for (int e = tid; e < s * s; e += blockDim.x) T[e] = G[e];
+    const double shift = mode == 1 ? 1e-11 : 0.0, pmin = mode == 1 ? 0.0 : 1e-10;
+    for (int e = tid; e < s * s; e += blockDim.x)
+      T[e] = (e / s == e % s) ? cmk(G[e].x + shift, G[e].y) : G[e];
     if (tid == 0) chol_ok = 1;
     __syncthreads();
     for (int k = 0; k < s; ++k) {
       const double dkk = T[k * s + k].x;
-      if (!(dkk >= 1e-10)) {
+      if (!(dkk >= pmin) || !(dkk > 0.0)) {
         if (tid == 0) chol_ok = 0;
         break;  // uniform across the block (all threads read the same dkk)
       }
@@ -958,7 +993,13 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   };
   // Z0 = unit vectors at the s largest diagonal entries of B (orthonormal by
   // construction; B e_i is the i-th column, rich in the dominant directions)
-  unit_start_kernel<<<1, 256, 0, st>>>(M, n, s, Z);
+  {
+    const int dyn_n = n <= 24 * 1024 ? n : 0;  // diagonal staged in smem up to 192 KB
+    if (dyn_n > 6 * 1024)
+      KST_CUDA(ctx, cudaFuncSetAttribute(unit_start_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(double) * dyn_n)));
+    unit_start_kernel<<<1, 1024, sizeof(double) * dyn_n, st>>>(M, n, s, Z, dyn_n);
+  }
   KST_LAUNCH(ctx);
   // Warm-up without Rayleigh-Ritz (Ritz pairs of the start block are useless):
   // Z <- orth(B^4 Z0), two orthonormalisation passes (SVQB when the block is

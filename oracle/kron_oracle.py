@@ -311,3 +311,25 @@ def pipeline(cube, ra, rb, n_doppler, n_spatial=16, tol=1e-4, max_iter=100,
     vals = detect(kind, ua, ub, cube, doppler_grid(n_doppler),
                   spatial_grid(p, n_spatial))
     return fit, ua, ub, vals
+
+
+def windowed(cube, n_w, ra, rb, n_doppler, n_spatial=16, tol=1e-4, max_iter=100,
+             kind="kron", bins=None):
+    """L-mode (SURVEY.md §8 "L-mode definition"; no reference equivalent): for
+    each test bin m, estimate on training bins [s, s + n_w) with
+    s = clamp(m - n_w // 2, 0, n_bins - n_w) and detect bin m with that
+    estimate. `bins` restricts the loop to a sample of test bins (rows of the
+    returned map outside it stay NaN)."""
+    n, p, q = cube.shape
+    dop, grid = doppler_grid(n_doppler), spatial_grid(p, n_spatial)
+    vals = np.full((n, n_doppler), np.nan)
+    fits = {}
+    for m in (range(n) if bins is None else bins):
+        s0 = min(max(m - n_w // 2, 0), n - n_w)
+        if s0 not in fits:
+            w = cube[s0:s0 + n_w]
+            fit = lrkron(scm(w.reshape(n_w, p * q), p, q), p, q, ra, rb, tol, max_iter)
+            fits[s0] = (fit, filter_bases(fit))
+        ua, ub = fits[s0][1]
+        vals[m] = detect(kind, ua, ub, cube[m:m + 1], dop, grid)[0]
+    return vals, {s0: f[0] for s0, f in fits.items()}

@@ -1,0 +1,77 @@
+"""L-mode: windowed Kron-STAP estimation (BASELINE.json configs[3]).
+
+The reference estimates one covariance from all bins of a frame; it has no
+windowed mode. SURVEY.md §8 ("L-mode definition") fixes the windowed variant
+as this loop over the reference's own functions: for each test bin m the
+training bins are [s, s + n_w) with s = clamp(m - n_w // 2, 0, n_bins - n_w),
+
+    est_m     = lr_kron_estimate(sample_covariance(cube_to_snapshots(cube[s:s+n_w]), p, q),
+                                 r_a, r_b)                         (src/lrkron.py:53, 118)
+    values[m] = detection_image(build_filter(kind, est_m), cube[m:m+1], dopplers,
+                                grid).values[0]                    (src/filters.py:137, 243)
+
+Here every step runs on the device (no host round trip of S or the cube):
+the n_bins - n_w + 1 distinct windows are estimated once each, and the bins
+that share a window (the first and last n_w // 2 + 1 bins share the edge
+windows) are detected together in one call.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DimensionError
+from .filters import DetectionMap, _host_grid_args, build_filter, run_detect
+from .layout import cube_to_snapshots
+from .lrkron import lr_kron_estimate, sample_covariance
+
+
+def window_start(m, n_w, n_bins):
+    """First training bin of test bin m: clamp(m - n_w // 2, 0, n_bins - n_w)."""
+    return int(min(max(m - n_w // 2, 0), n_bins - n_w))
+
+
+def window_bins(s, n_w, n_bins):
+    """Test bins [lo, hi) whose training window starts at s."""
+    h = n_w // 2
+    lo = 0 if s == 0 else s + h
+    hi = n_bins if s == n_bins - n_w else s + h + 1
+    return lo, hi
+
+
+def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, spatial_grid,
+                             kind="kron", tol=1e-4, max_iter=100, drop_temporal=False,
+                             return_estimates=False):
+    """Detection map of the windowed (L-mode) estimator; cube (n_bins, p, q).
+
+    Returns a DetectionMap (host arrays for numpy input, device tensor values
+    for CUDA input); with return_estimates=True also the list of
+    (window start, KronCovEstimate) pairs.
+    """
+    import torch
+    shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
+    if len(shp) != 3:
+        raise DimensionError(f"cube must be (n_bins, p, q), got {shp}")
+    n_bins, p, q = shp
+    if not 1 <= n_w <= n_bins:
+        raise DimensionError(f"window n_w={n_w} must be in [1, {n_bins}]")
+    x = nat.to_device(cube)
+    snaps = cube_to_snapshots(x)
+    dev_out = nat.is_device(cube)
+    D = int(np.asarray(dopplers.cpu() if nat.is_device(dopplers) else dopplers).size)
+    vals = torch.empty((n_bins, D), dtype=torch.float64, device=x.device)
+    ests = []
+    dop = grid = None
+    for s in range(n_bins - n_w + 1):
+        scm = sample_covariance(snaps[s:s + n_w], p, q)
+        est = lr_kron_estimate(scm, rank_spatial, rank_temporal, tol=tol, max_iter=max_iter)
+        filt = build_filter(kind, estimate=est, drop_temporal=drop_temporal)
+        if dop is None:
+            dop, grid = _host_grid_args(filt, dopplers, spatial_grid)
+        lo, hi = window_bins(s, n_w, n_bins)
+        vals[lo:hi] = run_detect(filt, x[lo:hi], dop, grid)[0]
+        if return_estimates:
+            ests.append((s, est))
+    dmap = DetectionMap(vals if dev_out else nat.to_host(vals), dop, grid)
+    return (dmap, ests) if return_estimates else dmap

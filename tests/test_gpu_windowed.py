@@ -1,0 +1,64 @@
+"""GPU parity of the L-mode windowed estimator (BASELINE.json configs[3],
+SURVEY.md §8 "L-mode definition") against the oracle's loop over the
+reference functions: per window identical iterations / convergence, maps
+within the §8c rule |v - v_ref| <= 1e-4 |v_ref| + 1e-5 M0."""
+
+import numpy as np
+import pytest
+
+from conftest import map_tolerance
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1604_03622_b200 as kst  # noqa: E402
+from oracle import kron_oracle as orc  # noqa: E402
+from paper_1604_03622_b200 import scenes  # noqa: E402
+
+
+def _m0(cube, D, G):
+    p = cube.shape[1]
+    return float(np.max(orc.detect("kron", None, None, cube, orc.doppler_grid(D),
+                                   orc.spatial_grid(p, G))))
+
+
+@pytest.mark.parametrize("n_w,ra,rb", [(9, 1, 3), (25, 1, 3), (9, 1, 1), (25, 2, 3)])
+def test_windowed_matches_oracle(n_w, ra, rb):
+    p, q, nb, D, G = 3, 64, 40, 64, 16
+    cube = scenes.bench_scene(p, q, nb, seed=17, movers=4).data[0]
+    ref, fits = orc.windowed(cube, n_w, ra, rb, D, G)
+    dmap, ests = kst.windowed_detection_image(cube, n_w, ra, rb, kst.make_doppler_grid(D),
+                                              kst.make_spatial_grid(p, G), return_estimates=True)
+    assert len(ests) == nb - n_w + 1 == len(fits)
+    for s, est in ests:
+        assert est.iterations == fits[s].iterations and est.converged == fits[s].converged
+        np.testing.assert_allclose(est.residuals, fits[s].residuals, rtol=1e-8, atol=1e-9)
+    m0 = _m0(cube, D, G)
+    err = np.abs(dmap.values - ref)
+    assert np.all(err <= map_tolerance(ref, m0)), (err / map_tolerance(ref, m0)).max()
+
+
+def test_windowed_cfg1_sampled_bins():
+    """configs[3] size (p=3, q=n_bins=D=256, G=16, n_w=81, ranks (1, 3)): full
+    GPU map, oracle on a seeded sample of bins (edges and interior)."""
+    p, q, nb, D, G, n_w = 3, 256, 256, 256, 16, 81
+    cube = scenes.bench_scene(p, q, nb, seed=17, movers=8).data[0]
+    bins = [0, 40, 41, 100, 173, 215, 216, 255]
+    ref, _ = orc.windowed(cube, n_w, 1, 3, D, G, bins=bins)
+    dmap = kst.windowed_detection_image(cube, n_w, 1, 3, kst.make_doppler_grid(D),
+                                        kst.make_spatial_grid(p, G))
+    m0 = _m0(cube, D, G)
+    got, want = dmap.values[bins], ref[bins]
+    assert np.all(np.abs(got - want) <= map_tolerance(want, m0))
+    assert np.all(np.isfinite(dmap.values)) and dmap.values.shape == (nb, D)
+
+
+def test_windowed_device_tensors_stay_on_device():
+    p, q, nb, D = 3, 32, 20, 32
+    cube = torch.from_numpy(scenes.bench_scene(p, q, nb, seed=5, movers=2).data[0]).cuda()
+    dmap = kst.windowed_detection_image(cube, 9, 1, 2, kst.make_doppler_grid(D),
+                                        kst.make_spatial_grid(p, 16))
+    assert dmap.values.is_cuda and tuple(dmap.values.shape) == (nb, D)

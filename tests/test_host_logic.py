@@ -121,3 +121,16 @@ def test_bench_reference_arm_prints_one_json_line():
     assert d["impl"] == "reference" and d["unit"] == "pixels/s" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "port"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_window_partition_covers_every_bin_once():
+    """L-mode windows: window_bins(s) are exactly the bins whose
+    window_start is s, and they partition [0, n_bins)."""
+    from paper_1604_03622_b200.windowed import window_bins, window_start
+    for n_bins, n_w in [(40, 9), (40, 25), (256, 81), (10, 10), (7, 1)]:
+        seen = []
+        for s in range(n_bins - n_w + 1):
+            lo, hi = window_bins(s, n_w, n_bins)
+            seen.extend(range(lo, hi))
+            assert all(window_start(m, n_w, n_bins) == s for m in range(lo, hi))
+        assert seen == list(range(n_bins))

@@ -117,9 +117,14 @@ __global__ void __launch_bounds__(128) bz_kernel(const cplx* __restrict__ B, int
 // element read once, 8 loads in flight per thread), Z rows broadcast from
 // shared memory. Split-K over blockIdx.y; partials summed in fixed order.
 constexpr int BZ2_COLS = 128;
+#ifndef KST_BZ2_K8
+#define KST_BZ2_K8 128
+#endif
 template <int S>
 struct Bz2K {
-  static constexpr int value = S <= 16 ? 128 : 64;  // keeps sz under 48 KB
+  // K chunk per CTA: more chunks = more CTAs in flight (B is L2-resident, the
+  // kernel is latency-bound); sz stays under 48 KB
+  static constexpr int value = S <= 8 ? KST_BZ2_K8 : S <= 16 ? 128 : 64;
 };
 template <int S>
 __global__ void __launch_bounds__(BZ2_COLS) bz2_kernel(const cplx* __restrict__ B, int n,
@@ -779,7 +784,7 @@ int ts_mul(TsCtx& t, const cplx* U, int ldu, int s1, const cplx* C, int ldc, int
 
 int bz(kst_ctx* ctx, const cplx* B, int n, const cplx* Z, int s, cplx* Y, cudaStream_t st) {
   if (s % 8 == 0 && s <= 32) {
-    const int kc = s <= 16 ? 128 : 64;
+    const int kc = s <= 8 ? KST_BZ2_K8 : s <= 16 ? 128 : 64;  // == Bz2K<s>
     const int ks = (n + kc - 1) / kc;
     cplx* part = (cplx*)ws_get(ctx, WS_BZ, sizeof(cplx) * (size_t)ks * n * s);
     if (!part) return set_err(ctx, KST_ERR_CUDA, "bz: workspace");

@@ -82,11 +82,13 @@ __device__ __forceinline__ uint8_t crt_residue8(int m, uint32_t h, uint32_t mid,
   return (uint8_t)(int8_t)(r >= 128u ? (int)r - m : (int)r);  // |r| <= 128
 }
 
-template <int NM, bool UNSIGNED>
+// NEG (two-SM tcgen05 path) adds a third part per modulus, -Xr' mod m.
+template <int NM, bool UNSIGNED, bool NEG>
 __global__ void __launch_bounds__(256) crt_residue_kernel(
     const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d, int64_t dpad,
     const int* __restrict__ expo, int beta, int8_t* __restrict__ R) {
-  __shared__ __align__(16) int8_t sb[NM][2][CR_A][CR_KP];
+  constexpr int NP = NEG ? 3 : 2;  // parts per modulus
+  __shared__ __align__(16) int8_t sb[NM][NP][CR_A][CR_KP];
   const int64_t a0 = (int64_t)blockIdx.x * CR_A;
   const int tid = threadIdx.x;
   const int c = tid & (CR_A - 1), r_first = tid / CR_A;
@@ -129,8 +131,10 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
                      li = (uint32_t)ui & 0xFFFFu;
 #pragma unroll
       for (int i = 0; i < NM; ++i) {
-        sb[i][0][c][r] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hr, mr, lr);
+        const uint8_t rr = crt_residue8<UNSIGNED>(modulus(i), hr, mr, lr);
+        sb[i][0][c][r] = (int8_t)rr;
         sb[i][1][c][r] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hi, mi, li);
+        if (NEG) sb[i][NP - 1][c][r] = (int8_t)(rr ? (uint8_t)(modulus(i) - rr) : (uint8_t)0);
       }
     }
     if (sub + 1 < CR_SUB) {  // prefetch the next sub-block
@@ -143,11 +147,11 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
     __syncthreads();
     const int64_t k = kb0 + 4 * lw;
     if (k < npad) {  // npad is a multiple of 16: whole words only
-      for (int seg = tid >> 4; seg < CR_A * NM * 2; seg += 16) {
-        const int cc = seg / (2 * NM), rem = seg % (2 * NM), i = rem >> 1, part = rem & 1;
+      for (int seg = tid >> 4; seg < CR_A * NM * NP; seg += 16) {
+        const int cc = seg / (NP * NM), rem = seg % (NP * NM), i = rem / NP, part = rem % NP;
         const int64_t aa = a0 + cc;
         if (aa >= dpad) continue;
-        *(uint32_t*)(R + (((size_t)aa * NM + i) * 2 + part) * npad + k) =
+        *(uint32_t*)(R + (((size_t)aa * NM + i) * NP + part) * npad + k) =
             *(const uint32_t*)&sb[i][part][cc][4 * lw];
       }
     }
@@ -352,14 +356,18 @@ const HostCrt& host_crt(int nmod) {
   return h;
 }
 
+// parts: 2 = {Xr', Xi'} (signed for cuBLAS, unsigned for the single-CTA
+// kernel), 3 = {Xr', Xi', -Xr'} unsigned (two-SM kernel)
 template <int NM>
 void launch_crt(const cplx* X, int64_t n, int64_t npad, int64_t d, int64_t dpad, const int* expo,
-                int beta, int8_t* R, bool uns, cudaStream_t st) {
+                int beta, int8_t* R, bool uns, int parts, cudaStream_t st) {
   const dim3 grid(cdiv(dpad, CR_A), cdiv(npad, CR_K * CR_SUB));
-  if (uns)
-    crt_residue_kernel<NM, true><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
+  if (parts == 3)
+    crt_residue_kernel<NM, true, true><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
+  else if (uns)
+    crt_residue_kernel<NM, true, false><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
   else
-    crt_residue_kernel<NM, false><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
+    crt_residue_kernel<NM, false, false><<<grid, 256, 0, st>>>(X, n, npad, d, dpad, expo, beta, R);
 }
 template <int NM>
 void launch_combine(const int32_t* GRe, const int32_t* GM, int64_t dpad, int64_t d, const int* expo,
@@ -596,6 +604,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
             }
             tc_fence_after();
             const uint32_t sa = smem_u32(base + s * TC_STAGE_BYTES);
+#ifdef KST_TC_INTERLEAVE
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 32; ++kk) {
               const uint64_t ar = sw128_desc(sa + 32 * kk);
@@ -608,6 +617,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
               tc_mma_i8(tmem + 128, ai, br, acc);    // M   = Xi_a Xr_b
               tc_mma_i8(tmem + 256, ar, bi, acc);    // MT  = Xr_a Xi_b
             }
+#else
+            // runs of MMAs into the same accumulator: Re (8), M (4), MT (4)
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 32; ++kk)  // Re = Xr_a Xr_b
+              tc_mma_i8(tmem, sw128_desc(sa + 32 * kk), sw128_desc(sa + 2 * TC_OPER + 32 * kk),
+                        (kb | kk) ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 32; ++kk)  //    + Xi_a Xi_b
+              tc_mma_i8(tmem, sw128_desc(sa + TC_OPER + 32 * kk),
+                        sw128_desc(sa + 3 * TC_OPER + 32 * kk), 1u);
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 32; ++kk)  // M = Xi_a Xr_b
+              tc_mma_i8(tmem + 128, sw128_desc(sa + TC_OPER + 32 * kk),
+                        sw128_desc(sa + 2 * TC_OPER + 32 * kk), (kb | kk) ? 1u : 0u);
+#pragma unroll
+            for (int kk = 0; kk < TC_BK / 32; ++kk)  // MT = Xr_a Xi_b
+              tc_mma_i8(tmem + 256, sw128_desc(sa + 32 * kk),
+                        sw128_desc(sa + 3 * TC_OPER + 32 * kk), (kb | kk) ? 1u : 0u);
+#endif
             tc_commit(&empty[s]);  // smem slot reusable once these MMAs retire
           }
           tc_commit(tfull);  // accumulators of modulus i complete
@@ -668,6 +696,246 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(TC_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- two-SM form
+// gram_tc2_kernel: the products on CTA pairs (cluster of 2, one CTA per SM)
+// with tcgen05.mma.cta_group::2, M = 256 and N = 256: work unit = rows
+// [256 I2, 256 I2 + 256) x columns [256 Jp, 256 Jp + 256), Jp >= I2. CTA rank
+// r holds its 128 rows of A (Xr', Xi' and the negated -Xr') and the 128 B rows
+// of column tile J = 2 Jp + r (Xr', Xi') in its own smem at the same offsets;
+// the leader (rank 0) issues every MMA for the pair and each CTA's TMEM
+// receives its 128 rows x 256 columns of two accumulators:
+//   Re += Ar.Br + Ai.Bi        Im += Ai.Br + An.Bi    (An = -Xr' mod m)
+// so Im = M - MT needs no third accumulator and TMEM (512 columns) holds
+// [Re | Im] for 256 columns. Per SM and 64-snapshot K block the operands are
+// 40 KB for 16 MMA units of 128 x 128 x 32 (2.5 KB per unit against 4 KB in
+// the single-CTA kernel: 40 B/clk per SM at full MMA rate, under the ~42 B/clk
+// the L2 delivers), and every instruction is a 256 x 256 MMA, which amortises
+// the per-instruction cost that holds the 128-wide MMAs at ~2/3 of the pipe
+// rate. Both CTAs' TMA loads complete on
+// the leader's full barrier (.cta_group::2); the leader's commits multicast
+// to both CTAs' empty / tfull barriers; both epilogues arrive on the leader's
+// tempty barrier. Sub-tiles below the diagonal (J < I) are computed and not
+// stored.
+#ifndef KST_TC2_BK
+#define KST_TC2_BK 64
+#endif
+constexpr int TC2_BK = KST_TC2_BK;               // K bytes per stage = swizzle row (64 or 128 B)
+constexpr int TC2_STAGES = TC2_BK == 64 ? 5 : 2;  // <= 200 KB of stages
+constexpr int TC2_TILE = TC_BM * TC2_BK;                    // 8 KB: 128 rows x 64 B
+constexpr int TC2_STAGE_BYTES = 5 * TC2_TILE;               // Ar, Ai, An | Br, Bi: 40 KB
+constexpr size_t TC2_SMEM = (size_t)TC2_STAGES * TC2_STAGE_BYTES + 1024 + 256;
+// kind::i8, D s32, A/B unsigned, K-major, N = 256, M = 256 (pair)
+constexpr uint32_t kTc2Idesc = (2u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA into this CTA's smem completing on an mbarrier of either CTA of the pair
+// (.cta_group::2 -- here always the leader's full barrier)
+__device__ __forceinline__ void tma_load3_to(const CUtensorMap* map, uint32_t mbar_cluster, void* dst,
+                                             int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(mbar_cluster), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+// K-major operand, 64B-swizzled rows of 64 bytes: 8-row groups 512 B apart;
+// with 128-byte rows the 128B-swizzled layout (sw128_desc)
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  if (TC2_BK == 128) return sw128_desc(saddr);
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)4 << 61);
+}
+__device__ __forceinline__ void tc2_mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kTc2Idesc), "r"(accumulate));
+}
+// arrive on the barrier at this smem offset in both CTAs once the issued MMAs retire
+__device__ __forceinline__ void tc2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) gram_tc2_kernel(
+    const __grid_constant__ CUtensorMap tmap, int T, int nunits, int nmod, int nkb,
+    uint8_t* __restrict__ res) {
+  extern __shared__ uint8_t tc_smem_raw[];
+  uint8_t* base = (uint8_t*)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(base + TC2_STAGES * TC2_STAGE_BYTES);
+  uint64_t* empty = full + TC2_STAGES;
+  uint64_t* tfull = empty + TC2_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = (uint32_t*)(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int T2 = T >> 1;  // pair tiles per side
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < TC2_STAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: one expect_tx arrival for both CTAs' bytes
+      mbar_init(&empty[s], 1);  // one multicast commit per use
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * TC_EPI_THREADS);  // both CTAs' epilogues (the leader's copy is used)
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "n"(TC_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      const uint32_t full_l0 = mapa_shared(&full[0], 0);
+      int it = 0;
+      for (int u = cid; u < nunits; u += ncl) {
+        int I2, Jp;
+        upper_tile(u, T2, I2, Jp);
+        const int arow = 256 * I2 + 128 * (int)rank, brow = 256 * Jp + 128 * (int)rank;
+        for (int i = 0; i < nmod; ++i)
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % TC2_STAGES;
+            const uint32_t ph = (uint32_t)(it / TC2_STAGES) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            uint8_t* st = base + s * TC2_STAGE_BYTES;
+            const uint32_t fb = full_l0 + (uint32_t)(s * sizeof(uint64_t));  // leader's full[s]
+            if (leader) mbar_expect_tx(&full[s], 2 * TC2_STAGE_BYTES);
+            const int k0 = kb * TC2_BK, pl = 3 * i;  // planes Xr', Xi', -Xr' of modulus i
+            tma_load3_to(&tmap, fb, st, k0, pl, arow);                     // Ar
+            tma_load3_to(&tmap, fb, st + TC2_TILE, k0, pl + 1, arow);      // Ai
+            tma_load3_to(&tmap, fb, st + 2 * TC2_TILE, k0, pl + 2, arow);  // An
+            tma_load3_to(&tmap, fb, st + 3 * TC2_TILE, k0, pl, brow);      // Br (this CTA's half)
+            tma_load3_to(&tmap, fb, st + 4 * TC2_TILE, k0, pl + 1, brow);  // Bi
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {  // ---------------- MMA issuer (leader only)
+      int it = 0, pass = 0;
+      for (int u = cid; u < nunits; u += ncl)
+        for (int i = 0; i < nmod; ++i, ++pass) {
+          mbar_wait(tempty, ((uint32_t)pass & 1u) ^ 1u);  // both epilogues drained TMEM
+          tc_fence_after();
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % TC2_STAGES;
+            const uint32_t ph = (uint32_t)(it / TC2_STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(base + s * TC2_STAGE_BYTES);
+            const uint32_t a_r = sa, a_i = sa + TC2_TILE, a_n = sa + 2 * TC2_TILE;
+            const uint32_t b_r = sa + 3 * TC2_TILE, b_i = sa + 4 * TC2_TILE;
+#pragma unroll
+            for (int kk = 0; kk < TC2_BK / 32; ++kk) {
+              const uint32_t acc = (kb | kk) ? 1u : 0u;
+              tc2_mma_i8(tmem, sw64_desc(a_r + 32 * kk), sw64_desc(b_r + 32 * kk), acc);  // Re
+              tc2_mma_i8(tmem, sw64_desc(a_i + 32 * kk), sw64_desc(b_i + 32 * kk), 1u);
+              tc2_mma_i8(tmem + 256, sw64_desc(a_i + 32 * kk), sw64_desc(b_r + 32 * kk), acc);  // Im
+              tc2_mma_i8(tmem + 256, sw64_desc(a_n + 32 * kk), sw64_desc(b_i + 32 * kk), 1u);
+            }
+            tc2_commit_both(&empty[s]);  // both CTAs' slot s reusable
+          }
+          tc2_commit_both(tfull);  // both CTAs' accumulators of modulus i complete
+        }
+    }
+  } else {  // ---------------- epilogue (both CTAs, own 128 rows x 256 columns)
+    // 16 warps: lane quarter q = warp % 4, column block cb = (warp - 2) / 4 of
+    // 64 columns = column tile J = 2 Jp + cb / 2, offset 64 (cb % 2); two
+    // rounds of 32 columns; TMEM is released after the second round's loads.
+    const int q = warp & 3, cb = (warp - 2) >> 2;
+    const int row = q * 32 + lane;
+    const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + 64 * cb;
+    const uint32_t tempty_l0 = mapa_shared(tempty, 0);
+    int pass = 0;
+    for (int u = cid; u < nunits; u += ncl) {
+      int I2, Jp;
+      upper_tile(u, T2, I2, Jp);
+      const int I = 2 * I2 + (int)rank, J = 2 * Jp + (cb >> 1);
+      const bool store = J >= I;
+      const int t = I * T - I * (I - 1) / 2 + (J - I);  // upper-tile index (when store)
+      for (int i = 0; i < nmod; ++i, ++pass) {
+        mbar_wait(tfull, (uint32_t)pass & 1u);
+        tc_fence_after();
+        const int m = c_tc_mod[i];
+        const uint32_t magic = c_tc_magic[i];
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          uint32_t vre[32], vim[32];
+          tc_ld32(taddr + 32 * h, vre);
+          tc_ld32(taddr + 256 + 32 * h, vim);
+          tc_wait_ld();
+          if (h == 1) {
+            tc_fence_before();
+            mbar_arrive_cluster(tempty_l0);  // this CTA's TMEM free for modulus i + 1
+          }
+          if (!store) continue;
+          uint32_t pre[8], pim[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            uint32_t a = 0, b = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = 4 * w + e;
+              a |= tc_mod((int)vre[j], m, magic) << (8 * e);
+              b |= tc_mod((int)vim[j], m, magic) << (8 * e);
+            }
+            pre[w] = a;
+            pim[w] = b;
+          }
+          uint8_t* out_re = res + (((size_t)t * nmod + i) * 2) * (TC_BM * TC_BM) +
+                            (size_t)row * TC_BM + 64 * (cb & 1) + 32 * h;
+          uint4* dre = (uint4*)out_re;
+          uint4* dim = (uint4*)(out_re + TC_BM * TC_BM);
+          dre[0] = make_uint4(pre[0], pre[1], pre[2], pre[3]);
+          dre[1] = make_uint4(pre[4], pre[5], pre[6], pre[7]);
+          dim[0] = make_uint4(pim[0], pim[1], pim[2], pim[3]);
+          dim[1] = make_uint4(pim[4], pim[5], pim[6], pim[7]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // the leader's last MMAs into the peer's TMEM have retired
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "n"(TC_TMEM_COLS)
                  : "memory");
   }
@@ -813,12 +1081,21 @@ static int scm_crt_tc(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S
                       cudaStream_t st) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return set_err(ctx, KST_ERR_CUDA, "scm_crt: cuTensorMapEncodeTiled unavailable");
+  // KST_TC2=1 selects the two-SM (cta_group::2, 256x256) kernel: same exact
+  // products, but measured ~5% slower end to end on B200 (3-plane residues,
+  // 256-row padding, below-diagonal sub-tiles) -- the single-CTA kernel runs
+  // at ~87% of the power-capped int8 rate already.
+  const char* tc2 = getenv("KST_TC2");
+  const bool pair = tc2 && atoi(tc2) == 1;
   const int64_t npad = ((n + 15) / 16) * 16;
-  const int64_t dpad = ((d + TC_BM - 1) / TC_BM) * TC_BM;
+  const int64_t dal = pair ? 2 * TC_BM : TC_BM;  // pair units span two row tiles
+  const int64_t dpad = ((d + dal - 1) / dal) * dal;
+  const int parts = pair ? 3 : 2;  // residue planes per modulus
   const int T = (int)(dpad / TC_BM);
   const int ntiles = T * (T + 1) / 2;
-  const int nkb = (int)((npad + TC_BK - 1) / TC_BK);
-  const int64_t ldr = (int64_t)nmod * 2 * npad;
+  const int bk = pair ? TC2_BK : TC_BK;
+  const int nkb = (int)((npad + bk - 1) / bk);
+  const int64_t ldr = (int64_t)nmod * parts * npad;
   char* sl = (char*)ws_get(ctx, WS_OZ_SLICES, (size_t)dpad * ldr + sizeof(int) * dpad + 256);
   uint8_t* res = (uint8_t*)ws_get(ctx, WS_OZ_PROD, (size_t)ntiles * nmod * 2 * TC_BM * TC_BM);
   if (!sl || !res) return set_err(ctx, KST_ERR_CUDA, "scm_crt: workspace");
@@ -837,12 +1114,13 @@ static int scm_crt_tc(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S
   }
   CUtensorMap map;
   {
-    const cuuint64_t dims[3] = {(cuuint64_t)npad, (cuuint64_t)(2 * nmod), (cuuint64_t)dpad};
+    const cuuint64_t dims[3] = {(cuuint64_t)npad, (cuuint64_t)(parts * nmod), (cuuint64_t)dpad};
     const cuuint64_t strides[2] = {(cuuint64_t)npad, (cuuint64_t)ldr};  // bytes, dims 1 and 2
-    const cuuint32_t box[3] = {TC_BK, 1, TC_BM};
+    const cuuint32_t box[3] = {(cuuint32_t)bk, 1, TC_BM};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)R, dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_err(ctx, KST_ERR_CUDA, "cuTensorMapEncodeTiled failed: %d", (int)r);
   }
@@ -855,8 +1133,34 @@ static int scm_crt_tc(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S
   }
   i8::colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
   KST_LAUNCH(ctx);
-  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, true, st)));
+  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, true, parts, st)));
   KST_LAUNCH(ctx);
+  if (pair) {
+    KST_CUDA(ctx, cudaFuncSetAttribute(gram_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)TC2_SMEM));
+    const int nunits = (T / 2) * (T / 2 + 1) / 2;  // upper 256 x 256 super-tiles
+    const int nclusters = std::min(nunits, nsm / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * nclusters));
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = TC2_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    stage_mark(ctx, 5, st);
+    KST_CUDA(ctx, cudaLaunchKernelEx(&cfg, gram_tc2_kernel, map, T, nunits, nmod, nkb, res));
+    KST_LAUNCH(ctx);
+    stage_mark(ctx, 6, st);
+    ctx->last_int8_ops = 2.0 * 4.0 * 4.0 * (double)TC_BM * TC_BM * (double)nkb * bk * nmod * nunits;
+    KST_CRT_DISPATCH(nmod, (launch_tile_combine<NM_>(res, T, ntiles, expo, beta, (double)n, d, S, st)));
+    KST_LAUNCH(ctx);
+    return KST_OK;
+  }
   KST_CUDA(ctx, cudaFuncSetAttribute(gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)TC_SMEM));
   stage_mark(ctx, 5, st);  // profiling: int8 tensor-core span (events 5..6)
@@ -941,7 +1245,7 @@ int scm_crt(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod
   }
   i8::colmax_kernel<<<cdiv(d, 32), dim3(32, 8), 0, st>>>(X, n, d, expo);
   KST_LAUNCH(ctx);
-  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, false, st)));
+  KST_CRT_DISPATCH(nmod, (launch_crt<NM_>(X, n, npad, d, dpad, expo, beta, R, false, 2, st)));
   KST_LAUNCH(ctx);
   stage_mark(ctx, 5, st);  // profiling: int8 GEMM span (events 5..6)
   const int32_t one = 1, zero = 0;

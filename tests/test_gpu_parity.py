@@ -297,6 +297,26 @@ def test_crt_tcgen05_kernel_matches_library_gemm_path(shape, nmod):
     assert (np.abs(s - ref) / dg).max() <= 1e-14
 
 
+@pytest.mark.parametrize("shape", [(3, 256, 256), (3, 100, 77), (2, 300, 1000), (3, 672, 2016)])
+def test_crt_pair_kernel_bit_identical(shape, monkeypatch):
+    """The two-SM cta_group::2 kernel (KST_TC2=1) and the single-CTA kernel
+    produce the same exact residue products, so S is bit-identical."""
+    from paper_1604_03622_b200 import lrkron
+    p, q, n = shape
+    rng = np.random.default_rng(11 + n)
+    snaps = rng.standard_normal((n, p * q)) + 1j * rng.standard_normal((n, p * q))
+    before = lrkron.get_gram_engine()
+    try:
+        lrkron.set_gram_engine("crt", 10)
+        monkeypatch.setenv("KST_TC2", "0")
+        ref = kst.sample_covariance(snaps, p, q).matrix
+        monkeypatch.setenv("KST_TC2", "1")
+        s = kst.sample_covariance(snaps, p, q).matrix
+    finally:
+        lrkron.set_gram_engine(*before)
+    np.testing.assert_array_equal(s, ref)
+
+
 @pytest.mark.parametrize("engine", [("int8", 6), ("crt", 10), ("crt-cublas", 10)])
 def test_int8_gram_propagates_non_finite_inputs(engine):
     from paper_1604_03622_b200 import lrkron

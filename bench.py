@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gotcha", choices=sorted(CONFIGS) + ["lmode"])
+    ap.add_argument("--config", default="gotcha", choices=sorted(CONFIGS) + ["lmode", "multipass"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -322,10 +322,103 @@ def run_lmode(args, rank, local, world):
                          "the eigen stages); the frame headline is configs[1]"}))
 
 
+def run_multipass(args, rank, local, world):
+    """Supplementary line for configs[4] (SURVEY.md §8 cfg 5): a 4-pass
+    3-channel 2001 x 2001 stack per GPU per step, stacked to (n, 12, q),
+    joint fit with ranks (K=4, 3) on the 24012 x 24012 covariance, one
+    filtering and 4 pass maps (kst_pipeline with groups = 4). Pixels are
+    pass-pixels (4 x n x D per frame). N > 1 runs independent stacks."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1604_03622_b200 as kst
+    from paper_1604_03622_b200 import _native as nat, scenes
+    from paper_1604_03622_b200.pipeline import process_frame_device
+    p, q, n, D, G, K, rb = 3, 2001, 2001, 2001, 16, 4, 3
+    hist = scenes.bench_scene(p, q, n, seed=17 + rank, movers=8, n_passes=K)
+    host = np.ascontiguousarray(kst.stack_passes(hist).data)  # (n, K p, q)
+    host_pin = torch.from_numpy(host).pin_memory()
+    cube = host_pin.to(dev)
+    dop, grid = kst.make_doppler_grid(D), kst.make_stacked_spatial_grid(p, K, G)
+    out = torch.empty((K, n, D), dtype=torch.float64, device=dev)
+    c = nat.ctx(dev)
+    for _ in range(args.warmup):
+        process_frame_device(cube, K, rb, dop, grid, groups=K, out=out)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    st = torch.cuda.current_stream(dev)
+    l0 = nat.lib().kst_launch_count(c)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        _, summ = process_frame_device(cube, K, rb, dop, grid, groups=K, out=out)
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    launches = nat.lib().kst_launch_count(c) - l0
+    # end to end: pinned host stack -> HBM, pipeline, maps -> pinned host, every step
+    hmaps = torch.empty((K, n, D), dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cube.copy_(host_pin, non_blocking=True)
+        process_frame_device(cube, K, rb, dop, grid, groups=K, out=out)
+        hmaps.copy_(out, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([ms, e2e_s * 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_s = float(t[0]), float(t[1]) / 1e3
+    if rank != 0:
+        return
+    px = K * n * D * world * args.steps
+    base = None
+    if not args.no_cpu_baseline:
+        # bounded sample: the reference path on a q = 251 stack of the same
+        # shape family (one full frame at q = 2001 needs a 9.2 GB S and ~2 min)
+        from oracle import kron_oracle as orc
+        qs = 251
+        sm = scenes.bench_scene(p, qs, qs, seed=17, movers=2, n_passes=K)
+        sd = orc.stack(sm.data)
+        tc = time.perf_counter()
+        fit = orc.lrkron(orc.scm(sd.reshape(qs, -1), K * p, qs), K * p, qs, K, rb)
+        ua, ub = orc.filter_bases(fit)
+        orc.pass_maps("kron", ua, ub, sd, K, p, orc.doppler_grid(qs), G)
+        tc = time.perf_counter() - tc
+        base = {"value": K * qs * qs / tc, "unit": "pixels/s", "cores": cpu_threads(),
+                "kind": "port",
+                "sample": f"one 4-pass stack at q = n_bins = D = {qs} through the oracle "
+                          "(scm, lrkron, bases, pass_maps); pass-pixels/s"}
+    print(json.dumps({
+        "metric": "STAP pass-pixels/sec", "value": px / (ms / 1e3), "unit": "pixels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128/f64",
+        "data": "synthetic (reference simulator restated in scenes.py; 4 passes, seeded, 8 movers)",
+        "config": {"workload": f"configs[4] multipass: K={K} passes x {n} bins x {D} Doppler, "
+                               f"p={p} (stacked {K * p}) q={q}, ranks ({K}, {rb}), "
+                               f"{G} spatial per pass; one stack per GPU per step",
+                   "K": K, "p": p, "q": q, "n_bins": n, "D": D, "G": G,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "iterations": int(summ[0])},
+        "e2e": {"value": px / e2e_s, "unit": "pixels/s",
+                "h2d_bytes_per_step": int(host.nbytes), "d2h_bytes_per_step": int(K * n * D * 8)},
+        "gpu_launches": int(launches), "cpu_baseline": base, "roofline": None,
+        "roofline_note": "supplementary line; the roofline is reported on the configs[1] headline"}))
+
+
 def main():
     args = parse()
     if args.config == "lmode" and args.impl == "ours":
         run_lmode(args, *dist_env())
+        return
+    if args.config == "multipass" and args.impl == "ours":
+        run_multipass(args, *dist_env())
         return
     cfg = CONFIGS[args.config]
     rank, local, world = dist_env()

@@ -181,6 +181,13 @@ __device__ __forceinline__ double crt_finish(double s0, double s1, double s2) {
 // powers 2^(sh/2), 2^(sh - sh/2) (each a normal double for |sh| <= 2044), then
 // the quotient by one Newton correction of v (1/n) (within an ulp of the
 // correctly rounded v / n; no FP64 divide or ldexp per entry)
+// |sh| > 1022 (extreme column scales): out of line, so the common path is
+// not predicated through ldexp's instruction sequence
+__device__ __noinline__ double crt_scale_far(double v, int sh, double dn, double rn) {
+  const double x = ldexp(v, sh);
+  const double q = x * rn;
+  return fma(fma(-q, dn, x), rn, q);
+}
 __device__ __forceinline__ double crt_scale(double v, int sh, double dn, double rn) {
 #ifdef KST_SCALE_SPLIT
   sh = max(-2044, min(2046, sh));
@@ -188,9 +195,8 @@ __device__ __forceinline__ double crt_scale(double v, int sh, double dn, double 
   const double x = v * __longlong_as_double((long long)(h1 + 1023) << 52) *
                    __longlong_as_double((long long)(h2 + 1023) << 52);
 #else  // measured faster (A/B, tools/ab_kernels.sh)
-  const double x = (sh >= -1022 && sh <= 1023)
-                       ? v * __longlong_as_double((long long)(sh + 1023) << 52)
-                       : ldexp(v, sh);
+  if (sh < -1022 || sh > 1023) return crt_scale_far(v, sh, dn, rn);
+  const double x = v * __longlong_as_double((long long)(sh + 1023) << 52);
 #endif
   const double q = x * rn;
   return fma(fma(-q, dn, x), rn, q);
@@ -1026,10 +1032,172 @@ __global__ void __launch_bounds__(256, 2) crt_tile_combine_kernel(
   }
 }
 
+// Strip variant (default): persistent CTAs, item = (tile, 8-row strip). A
+// producer lane streams each item's 2 NM residue planes (8 rows x 128 B =
+// 1 KB, contiguous) into an mbarrier ring with bulk async copies, so the
+// loads run ahead of the FP64 reconstruction instead of stalling it (the
+// per-thread-load kernel above spends most of its time on long-scoreboard
+// waits at 25 % occupancy). 8 consumer warps: row r = warp, 4 columns per
+// lane; S rows (2 KB segments) and the conjugate mirror (128 B segments)
+// are written from an smem transpose.
+constexpr int CS_ROWS = 8, CS_CONS = 256;
+#ifndef KST_CS_STAGES
+#define KST_CS_STAGES 2
+#endif
+// 2 stages x 20 KB: three CTAs per SM (A/B: 232 us vs 247 us at 4 stages, 2 CTAs)
+__host__ __device__ constexpr int cs_stages(int nm) { return nm <= 10 ? KST_CS_STAGES : 2; }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cons_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(CS_CONS) : "memory");
+}
+
+template <int NM>
+__global__ void __launch_bounds__(CS_CONS + 32, 3) crt_strip_combine_kernel(
+    const uint8_t* __restrict__ res, int T, int nitems, const int* __restrict__ expo, int beta,
+    double dn, int64_t d, cplx* __restrict__ S) {
+  constexpr int PLANE = CS_ROWS * TC_BM, STAGE = 2 * NM * PLANE, NS = cs_stages(NM);
+  constexpr int VLD = TC_BM + 1;  // padded vt row (conflict-free column reads)
+  extern __shared__ __align__(128) unsigned char cs_smem[];
+  __shared__ uint64_t full[NS], empty[NS];
+  uint8_t* ring = cs_smem;
+  cplx* vt = (cplx*)(cs_smem + NS * STAGE);  // [CS_ROWS][VLD]
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CS_CONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  constexpr int SPT = TC_BM / CS_ROWS;  // strips per tile
+  if (tid >= CS_CONS) {  // ------------------------------ producer lane
+    if (tid == CS_CONS) {
+      int it = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+        const int s = it % NS;
+        mbar_wait(&empty[s], ((uint32_t)(it / NS) & 1u) ^ 1u);
+        mbar_expect_tx(&full[s], STAGE);
+        const uint8_t* src = res + (size_t)(item / SPT) * NM * 2 * (TC_BM * TC_BM) +
+                             (size_t)(item % SPT) * PLANE;
+        for (int pl = 0; pl < 2 * NM; ++pl)
+          bulk_load(ring + s * STAGE + pl * PLANE, src + (size_t)pl * (TC_BM * TC_BM), PLANE, &full[s]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------ consumers
+  constexpr int NCH = crt_nch(NM);
+  const double rn = 1.0 / dn;
+  const int r = tid >> 5, l = tid & 31;
+  int it = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+    const int s = it % NS;
+    const int t = item / SPT;
+    int I, J;
+    upper_tile(t, T, I, J);
+    const int64_t a0 = (int64_t)I * TC_BM + (item % SPT) * CS_ROWS, b0 = (int64_t)J * TC_BM;
+    const int64_t a = a0 + r;
+    // column exponents first: their global latency overlaps the ring wait
+    const int ea = (a < d) ? __ldg(&expo[a]) : 0;
+    int eb[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) eb[c] = (b0 + 4 * l + c < d) ? __ldg(&expo[b0 + 4 * l + c]) : 0;
+    mbar_wait(&full[s], (uint32_t)(it / NS) & 1u);
+    uint32_t pr[NM], pm[NM];
+    const uint8_t* src = ring + s * STAGE + r * TC_BM + 4 * l;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      pr[i] = *(const uint32_t*)(src + (2 * i) * PLANE);
+      pm[i] = *(const uint32_t*)(src + (2 * i + 1) * PLANE);
+    }
+    __syncwarp();
+    if (l == 0) mbar_arrive(&empty[s]);  // residues are in registers: release the slot
+    double re0[4], re1[4], re2[4], im0[4], im1[4], im2[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) re0[c] = re1[c] = re2[c] = im0[c] = im1[c] = im2[c] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      const double w0 = c_crt.w[i][0], w1 = c_crt.w[i][1], w2 = c_crt.w[i][2];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t cr = __byte_perm(pr[i], 0, 0x4440 + c), cm = __byte_perm(pm[i], 0, 0x4440 + c);
+        const double dr = __longlong_as_double(0x4330000000000000ll | cr) - 4503599627370496.0;
+        const double dm = __longlong_as_double(0x4330000000000000ll | cm) - 4503599627370496.0;
+        re0[c] = fma(dr, w0, re0[c]);
+        re1[c] = fma(dr, w1, re1[c]);
+        im0[c] = fma(dm, w0, im0[c]);
+        im1[c] = fma(dm, w1, im1[c]);
+        if (NCH == 3) {
+          re2[c] = fma(dr, w2, re2[c]);
+          im2[c] = fma(dm, w2, im2[c]);
+        }
+      }
+    }
+    cons_sync();  // previous item's vt reads are done
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      cplx v;
+      if (ea == kNaNExpo || eb[c] == kNaNExpo) {
+        v = cmk(NAN, NAN);
+      } else {
+        const int sh = ea + eb[c] - 2 * beta;
+        v = cmk(crt_scale(crt_finish<NCH>(re0[c], re1[c], re2[c]), sh, dn, rn),
+                crt_scale(crt_finish<NCH>(im0[c], im1[c], im2[c]), sh, dn, rn));
+      }
+      vt[r * VLD + 4 * l + c] = v;
+    }
+    cons_sync();
+    // S[a][b], a <= b: one 2 KB row segment per warp trip
+#pragma unroll
+    for (int k = 0; k < CS_ROWS * TC_BM / CS_CONS; ++k) {
+      const int idx = tid + k * CS_CONS, rr = idx >> 7, cc = idx & (TC_BM - 1);
+      const int64_t aa = a0 + rr, bb = b0 + cc;
+      if (aa < d && bb < d && aa <= bb) {
+        const cplx v = vt[rr * VLD + cc];
+        S[aa * d + bb] = (aa == bb) ? cmk(v.x, 0.0) : v;
+      }
+    }
+    // S[b][a] = conj(S[a][b]), a < b: 128 B row segments
+#pragma unroll
+    for (int k = 0; k < CS_ROWS * TC_BM / CS_CONS; ++k) {
+      const int idx = tid + k * CS_CONS, cc = idx / CS_ROWS, rr = idx % CS_ROWS;
+      const int64_t aa = a0 + rr, bb = b0 + cc;
+      if (aa < d && bb < d && aa < bb) {
+        const cplx v = vt[rr * VLD + cc];
+        S[bb * d + aa] = cmk(v.x, -v.y);
+      }
+    }
+  }
+}
+
 template <int NM>
 void launch_tile_combine(const uint8_t* res, int T, int ntiles, const int* expo, int beta, double dn,
                          int64_t d, cplx* S, cudaStream_t st) {
-  crt_tile_combine_kernel<NM><<<(unsigned)ntiles * 16, 256, 0, st>>>(res, T, expo, beta, dn, d, S);
+  static const bool strip = !(getenv("KST_CTC") && atoi(getenv("KST_CTC")) == 0);
+  if (!strip) {
+    crt_tile_combine_kernel<NM><<<(unsigned)ntiles * 16, 256, 0, st>>>(res, T, expo, beta, dn, d, S);
+    return;
+  }
+  constexpr int smem = cs_stages(NM) * 2 * NM * CS_ROWS * TC_BM + CS_ROWS * (TC_BM + 1) * 16;
+  static int grid = 0;
+  if (!grid) {
+    int dev = 0, nsm = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(crt_strip_combine_kernel<NM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, crt_strip_combine_kernel<NM>, CS_CONS + 32, smem);
+    grid = nsm * std::max(per, 1);
+  }
+  const int nitems = ntiles * (TC_BM / CS_ROWS);
+  crt_strip_combine_kernel<NM><<<(unsigned)std::min(grid, nitems), CS_CONS + 32, smem, st>>>(
+      res, T, nitems, expo, beta, dn, d, S);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,

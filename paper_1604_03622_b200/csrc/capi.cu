@@ -4,6 +4,8 @@
 #include <cstdarg>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -38,6 +40,23 @@ void* ws_get(kst_ctx* ctx, int slot, size_t bytes) {
   }
   s.bytes = want;
   return s.ptr;
+}
+
+int const_upload(kst_ctx* ctx, const void* symbol, const void* src, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, std::vector<char>> held;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto& cur = held[{dev, symbol}];
+  if (cur.size() == bytes && std::memcmp(cur.data(), src, bytes) == 0) return KST_OK;
+  const cudaError_t e = cudaMemcpyToSymbolAsync(symbol, src, bytes, 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) {
+    cur.clear();
+    return set_err(ctx, KST_ERR_CUDA, "constant upload: %s", cudaGetErrorString(e));
+  }
+  cur.assign((const char*)src, (const char*)src + bytes);
+  return KST_OK;
 }
 
 void* pinned_get(kst_ctx* ctx, size_t bytes) {
@@ -269,7 +288,8 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   }
   stage_mark(ctx, 3, st);
   KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, ka ? ua : nullptr, ka, kb ? ub : nullptr, kb,
-                      kind, 0, dopplers, D, (const cplx*)grid, G, groups, values, st));
+                      kind, 0, dopplers, D, (const cplx*)grid, G, groups, values, st,
+                      /*check_finite=*/false));  // a non-finite cube already failed lrkron
   stage_mark(ctx, 4, st);
   if (summary) {
     summary[0] = fit.iterations;

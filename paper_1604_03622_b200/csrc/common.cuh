@@ -74,6 +74,10 @@ struct kst_ctx {
   double last_int8_ops = 0.0;  // int8 ops issued by the last int8 Gram (bench roofline)
   // instrumentation: kernel launches issued, and per-stage CUDA events of the
   // last kst_pipeline call (recorded only when profiling is on)
+  // detection constants resident in the WS_DET workspace (conj grid,
+  // Dopplers, twiddles): the key they were uploaded for
+  const void* det_base = nullptr;
+  std::vector<double> det_key;
   long long launches = 0;
   int profiling = 0;
   cudaEvent_t ev[8] = {};
@@ -113,6 +117,12 @@ enum WsSlot {
 
 void* ws_get(kst_ctx* ctx, int slot, size_t bytes);  // may return nullptr on OOM
 void* pinned_get(kst_ctx* ctx, size_t bytes);
+// Upload `bytes` of host data to a __constant__ `symbol` on the current
+// device unless it already holds exactly these bytes (constant plans are
+// device-global; repeated frames with the same plan skip the small
+// host->device transfer, which costs tens of us when PCIe is saturated by a
+// cube upload).
+int const_upload(kst_ctx* ctx, const void* symbol, const void* src, size_t bytes, cudaStream_t st);
 
 int set_err(kst_ctx* ctx, int code, const char* fmt, ...);
 
@@ -245,5 +255,6 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
 // detect.cu
 int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
            const cplx* ub, int kb, int kind, int spatial_only, const double* dop_host, int D,
-           const cplx* grid_host, int G, int groups, double* values, cudaStream_t st);
+           const cplx* grid_host, int G, int groups, double* values, cudaStream_t st,
+           bool check_finite = true);
 }  // namespace kst

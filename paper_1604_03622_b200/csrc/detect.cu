@@ -25,6 +25,9 @@
 
 namespace {
 
+#ifndef KST_FFT_GRP
+#define KST_FFT_GRP 0
+#endif
 constexpr int NT = 256;
 constexpr int kMaxFactors = 32;
 constexpr int kMaxP = 16;
@@ -103,6 +106,79 @@ __device__ __forceinline__ void stage_reg(const cplx* __restrict__ a, cplx* __re
   }
 }
 
+// Large odd radices (11, 13, 23, 29) in two phases, so the R-point
+// butterflies neither pin 2R doubles per thread nor leave most threads idle
+// (the radix-29 stage of D = 2001 has only 69 butterflies):
+//   A (one thread per butterfly j): twiddled t_r, pairs s_r = t_r + t_{R-r},
+//     d_r = t_r - t_{R-r} written back in place, X_0 = t_0 + sum s_r;
+//   B (one thread per (j, group of GU output pairs)): streams (s_r, d_r)
+//     from smem and keeps 4 GU independent accumulator chains in registers.
+// Same operation order per output as stage_reg (bitwise identical results).
+template <int R, int GU, int G>
+__device__ __forceinline__ void grp_unit(const cplx* __restrict__ a, cplx* __restrict__ b, int j,
+                                         int DR, int Ns) {
+  constexpr int h = (R - 1) / 2, off = rtw_off(R);
+  constexpr int U0 = 1 + G * GU, U1 = (U0 + GU - 1 < h) ? U0 + GU - 1 : h, NU = U1 - U0 + 1;
+  const int k = j % Ns, dst = (j / Ns) * Ns * R + k;
+  const cplx t0 = a[j];
+  double ax[NU], ay[NU], bx[NU], by[NU];
+#pragma unroll
+  for (int v = 0; v < NU; ++v) {
+    ax[v] = t0.x;
+    ay[v] = t0.y;
+    bx[v] = 0.0;
+    by[v] = 0.0;
+  }
+#pragma unroll
+  for (int r = 1; r <= h; ++r) {
+    const cplx sr = a[j + r * DR], dr = a[j + (R - r) * DR];
+#pragma unroll
+    for (int v = 0; v < NU; ++v) {
+      const int m = (r * (U0 + v)) % R;
+      const double wc = c_plan.rtw[2 * (off + m)], ws = c_plan.rtw[2 * (off + m) + 1];
+      ax[v] = fma(wc, sr.x, ax[v]);
+      ay[v] = fma(wc, sr.y, ay[v]);
+      bx[v] = fma(-ws, dr.x, bx[v]);
+      by[v] = fma(-ws, dr.y, by[v]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NU; ++v) {
+    const int u = U0 + v;
+    b[dst + u * Ns] = cmk(ax[v] + by[v], ay[v] - bx[v]);        // A - iB
+    b[dst + (R - u) * Ns] = cmk(ax[v] - by[v], ay[v] + bx[v]);  // A + iB
+  }
+}
+
+template <int R, int GU>
+__device__ void stage_grp(cplx* __restrict__ a, cplx* __restrict__ b, const cplx* __restrict__ w,
+                          int D, int Ns) {
+  constexpr int h = (R - 1) / 2, NGR = (h + GU - 1) / GU;
+  static_assert(NGR >= 1 && NGR <= 3, "stage_grp: 1..3 output groups");
+  const int DR = D / R, step = D / (Ns * R);
+  for (int j = threadIdx.x; j < DR; j += blockDim.x) {  // phase A
+    const int k = j % Ns, dst = (j / Ns) * Ns * R + k;
+    cplx x0 = a[j];
+#pragma unroll
+    for (int r = 1; r <= h; ++r) {
+      const cplx tr = cmul(a[j + r * DR], w[r * k * step]);
+      const cplx tm = cmul(a[j + (R - r) * DR], w[(R - r) * k * step]);
+      const cplx sr = cadd(tr, tm);
+      a[j + r * DR] = sr;
+      a[j + (R - r) * DR] = csub(tr, tm);
+      x0 = cadd(x0, sr);
+    }
+    b[dst] = x0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < DR * NGR; e += blockDim.x) {  // phase B
+    const int j = e % DR, g = e / DR;
+    if (g == 0) grp_unit<R, GU, 0>(a, b, j, DR, Ns);
+    if (NGR > 1 && g == 1) grp_unit<R, GU, (NGR > 1 ? 1 : 0)>(a, b, j, DR, Ns);
+    if (NGR > 2 && g == 2) grp_unit<R, GU, (NGR > 2 ? 2 : 0)>(a, b, j, DR, Ns);
+  }
+}
+
 // Ping-pong Stockham DFT (decimation in time) of length D over shared
 // buffers; w[k] = exp(-2 pi i k / D). Stage (radix R, Ns = product of the
 // previous radices, DR = D / R, step = D / (Ns R)), for j < DR, k = j mod Ns:
@@ -148,10 +224,17 @@ __device__ cplx* stockham(cplx* a, cplx* b, const cplx* __restrict__ w, int D) {
         case 3: stage_reg<3>(a, b, w, D, Ns); break;
         case 5: stage_reg<5>(a, b, w, D, Ns); break;
         case 7: stage_reg<7>(a, b, w, D, Ns); break;
+#if KST_FFT_GRP
+        case 11: stage_grp<11, 5>(a, b, w, D, Ns); break;
+        case 13: stage_grp<13, 6>(a, b, w, D, Ns); break;
+        case 23: stage_grp<23, 6>(a, b, w, D, Ns); break;
+        default: stage_grp<29, 7>(a, b, w, D, Ns); break;
+#else
         case 11: stage_reg<11>(a, b, w, D, Ns); break;
         case 13: stage_reg<13>(a, b, w, D, Ns); break;
         case 23: stage_reg<23>(a, b, w, D, Ns); break;
         default: stage_reg<29>(a, b, w, D, Ns); break;
+#endif
       }
     } else {
       const int h = (R - 1) / 2;
@@ -213,8 +296,20 @@ __device__ cplx* stockham(cplx* a, cplx* b, const cplx* __restrict__ w, int D) {
 // coefficients against U_B and the folded DFT (uniform) or direct sum.
 // 128-thread CTAs: the register-resident radix-23/29 butterflies need ~150
 // registers, so two row-CTAs per SM beat one 256-thread CTA.
-constexpr int NTS = 128;
-__global__ void __launch_bounds__(NTS) row_spectrum_kernel(
+#ifndef KST_NTS
+#define KST_NTS 128
+#endif
+constexpr int NTS = KST_NTS;
+#ifndef KST_RS_GTW
+#define KST_RS_GTW 0
+#endif
+#ifndef KST_RS_MINB
+#define KST_RS_MINB 1
+#endif
+#ifndef KST_CB_MINB
+#define KST_CB_MINB 1
+#endif
+__global__ void __launch_bounds__(NTS, KST_RS_MINB) row_spectrum_kernel(
     const cplx* __restrict__ src, int64_t rows, int q, const cplx* __restrict__ ub, int kb,
     const cplx* __restrict__ w, int D, int uniform, const double* __restrict__ dop,
     cplx* __restrict__ spec, cplx* __restrict__ coef, int* __restrict__ nonfinite) {
@@ -231,10 +326,15 @@ __global__ void __launch_bounds__(NTS) row_spectrum_kernel(
   const bool staged_fft = uniform && q <= D;
   cplx* xs = smem;  // staged row (both paths start at smem[0])
   if (uniform) {
+#if KST_RS_GTW
+    for (int k = threadIdx.x; k < D; k += NT) {
+      if (staged_fft) {
+#else
     cplx* tw = smem + 2 * D;
     for (int k = threadIdx.x; k < D; k += NT) {
       cp_async16(&tw[k], &w[k]);
       if (staged_fft) {
+#endif
         if (k < q)
           cp_async16(&xs[k], &x[k]);
         else
@@ -293,7 +393,11 @@ __global__ void __launch_bounds__(NTS) row_spectrum_kernel(
   if (uniform) {
     cplx* a = smem;
     cplx* b = smem + D;
+#if KST_RS_GTW
+    const cplx* tw = w;  // twiddle table read through L1 (frees 1/3 of the smem)
+#else
     cplx* tw = smem + 2 * D;
+#endif
     if (staged_fft) {
       for (int t = threadIdx.x; t < q; t += NT) {
         const cplx v = a[t];
@@ -332,7 +436,7 @@ __global__ void __launch_bounds__(NTS) row_spectrum_kernel(
       spec[row * D + d] = acc;
     }
   }
-  if (bad) atomicOr(nonfinite, 1);
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
 }
 
 // Transpose U_B (q x kb) into kb rows of length q.
@@ -358,7 +462,7 @@ struct CombineArgs {
 // per-pixel channel loops are fully unrolled in registers.
 constexpr int CB_BINS = 8;
 template <int PT>
-__global__ void __launch_bounds__(NT) combine_kernel(
+__global__ void __launch_bounds__(NT, KST_CB_MINB) combine_kernel(
     const cplx* __restrict__ spec, const cplx* __restrict__ coef, const cplx* __restrict__ ubspec,
     const cplx* __restrict__ ua, const cplx* __restrict__ hconj, CombineArgs a,
     double* __restrict__ values, int64_t n) {
@@ -584,7 +688,8 @@ namespace kst {
 
 int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
            const cplx* ub, int kb, int kind, int spatial_only, const double* dop_host, int D,
-           const cplx* grid_host, int G, int groups, double* values, cudaStream_t st) {
+           const cplx* grid_host, int G, int groups, double* values, cudaStream_t st,
+           bool check_finite) {
   if (p < 1 || q < 1 || D < 1 || G < 1 || groups < 1 || G % groups)
     return set_err(ctx, KST_ERR_DIMENSION, "detect: bad shape p=%d q=%d D=%d G=%d groups=%d", p, q,
                    D, G, groups);
@@ -621,19 +726,33 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   double* dop = (double*)(hconj + (size_t)G * p);
   int* flag = (int*)(dop + D);
 
-  // host staging of conj(grid) and dopplers
-  for (int e = 0; e < G * p; ++e) hstage[e] = cconj(grid_host[e]);
-  double* hdop = (double*)(hstage + (size_t)G * p);
-  for (int d = 0; d < D; ++d) hdop[d] = dop_host[d];
-  KST_CUDA(ctx, cudaMemcpyAsync(hconj, hstage, sizeof(cplx) * G * p, cudaMemcpyHostToDevice, st));
-  KST_CUDA(ctx, cudaMemcpyAsync(dop, hdop, sizeof(double) * D, cudaMemcpyHostToDevice, st));
-  KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));
-  if (uniform) {
-    KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_plan, &plan, sizeof(Plan), 0, cudaMemcpyHostToDevice, st));
-    twiddle_kernel<<<cdiv(D, 256), 256, 0, st>>>(tw, D);
-    KST_LAUNCH(ctx);
+  // conj(grid), Dopplers and the twiddle table stay resident in the
+  // workspace: re-uploaded only when the grid, the layout or the buffer change
+  std::vector<double> key;
+  key.reserve(8 + D + 2 * (size_t)G * p);
+  for (double v : {(double)D, (double)G, (double)p, (double)q, (double)kb_used, (double)uniform,
+                   (double)rows})
+    key.push_back(v);
+  key.insert(key.end(), dop_host, dop_host + D);
+  key.insert(key.end(), (const double*)grid_host, (const double*)grid_host + 2 * (size_t)G * p);
+  if (ctx->det_base != base || ctx->det_key != key) {
+    for (int e = 0; e < G * p; ++e) hstage[e] = cconj(grid_host[e]);
+    double* hdop = (double*)(hstage + (size_t)G * p);
+    for (int d = 0; d < D; ++d) hdop[d] = dop_host[d];
+    KST_CUDA(ctx, cudaMemcpyAsync(hconj, hstage, sizeof(cplx) * G * p, cudaMemcpyHostToDevice, st));
+    KST_CUDA(ctx, cudaMemcpyAsync(dop, hdop, sizeof(double) * D, cudaMemcpyHostToDevice, st));
+    if (uniform) {
+      twiddle_kernel<<<cdiv(D, 256), 256, 0, st>>>(tw, D);
+      KST_LAUNCH(ctx);
+    }
+    // the staging buffer is reused by the next call: wait for the copies
+    KST_CUDA(ctx, cudaStreamSynchronize(st));
+    ctx->det_base = base;
+    ctx->det_key.swap(key);
   }
-  const size_t smem = uniform ? sizeof(cplx) * 3 * D : sizeof(cplx) * q;
+  if (uniform) KST_TRY(const_upload(ctx, (const void*)&c_plan, &plan, sizeof(Plan), st));
+  if (check_finite) KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));
+  const size_t smem = uniform ? sizeof(cplx) * (KST_RS_GTW ? 2 : 3) * D : sizeof(cplx) * q;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     KST_CUDA(ctx, cudaFuncSetAttribute(row_spectrum_kernel,
@@ -649,7 +768,8 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
     KST_LAUNCH(ctx);
   }
   row_spectrum_kernel<<<(unsigned)rows, NTS, smem, st>>>(cube, rows, q, ub, kb_used, tw, D, uniform,
-                                                        dop, spec, coef, flag);
+                                                        dop, spec, coef,
+                                                        check_finite ? flag : nullptr);
   KST_LAUNCH(ctx);
   CombineArgs a;
   a.P = p;
@@ -665,6 +785,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
                                           sizeof(cplx) * G * p, st>>>(
                         spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n)));
   KST_LAUNCH(ctx);
+  if (!check_finite) return KST_OK;
   int hflag = 0;
   KST_CUDA(ctx, cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   KST_CUDA(ctx, cudaStreamSynchronize(st));
@@ -685,6 +806,7 @@ int filter_cube(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const c
   const int64_t rows = n * p;
   char* base = (char*)ws_get(ctx, WS_DET, sizeof(cplx) * (size_t)rows * std::max(kb_used, 1) + 256);
   if (!base) return set_err(ctx, KST_ERR_CUDA, "filter: workspace");
+  ctx->det_base = nullptr;  // overwrites detect's resident grid / twiddles
   cplx* coef = (cplx*)base;
   int* flag = (int*)(coef + (size_t)rows * std::max(kb_used, 1));
   KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));

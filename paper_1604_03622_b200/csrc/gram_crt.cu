@@ -1277,8 +1277,8 @@ static int scm_crt_tc(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S
       magic[i] = kModuli[i] == 256 ? (1u << 31)
                                    : (uint32_t)((((uint64_t)1 << 39) + kModuli[i] - 1) / kModuli[i]);
     }
-    KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_tc_mod, mods, sizeof(mods), 0, cudaMemcpyHostToDevice, st));
-    KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_tc_magic, magic, sizeof(magic), 0, cudaMemcpyHostToDevice, st));
+    KST_TRY(const_upload(ctx, (const void*)&c_tc_mod, mods, sizeof(mods), st));
+    KST_TRY(const_upload(ctx, (const void*)&c_tc_magic, magic, sizeof(magic), st));
   }
   CUtensorMap map;
   {
@@ -1369,7 +1369,7 @@ int scm_crt(kst_ctx* ctx, const cplx* X, int64_t n, int64_t d, cplx* S, int nmod
   if (2 * n > (int64_t)1 << 17)
     return set_err(ctx, KST_ERR_DIMENSION, "CRT Gram: int32 products need n <= 65536");
   const HostCrt& hc = host_crt(nmod);
-  KST_CUDA(ctx, cudaMemcpyToSymbolAsync(c_crt, &hc.c, sizeof(CrtConst), 0, cudaMemcpyHostToDevice, st));
+  KST_TRY(const_upload(ctx, (const void*)&c_crt, &hc.c, sizeof(CrtConst), st));
   // n > kTcMaxN (beyond every configuration here) takes the library-GEMM form
   // of the same numerics
   if (use_tc && n <= kTcMaxN) return scm_crt_tc(ctx, X, n, d, S, nmod, beta, st);

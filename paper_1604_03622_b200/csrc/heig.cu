@@ -957,12 +957,12 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   const size_t nb = (size_t)n * s;
   const int nblk = std::min((n + K4_ROWS - 1) / K4_ROWS, 32);
   const int nup = (n + 7) / 8;
-  size_t bytes = sizeof(cplx) * (nb * 5 + (size_t)s * s * 2) + sizeof(double) * (2 * s) +
-                 sizeof(int) * 8 + 256;
+  size_t bytes = sizeof(cplx) * (nb * 5 + (size_t)s * s * 2) +
+                 sizeof(double) * ((size_t)nup * r + 2 * s) + sizeof(int) * 8 + 256;
   char* base = (char*)ws_get(ctx, WS_EIG, bytes);
   cplx* partial = (cplx*)ws_get(ctx, WS_EIG2, sizeof(cplx) * (size_t)nblk * 2 * s * s +
                                                   sizeof(double) * (size_t)nup * r + 64);
-  double* hres = (double*)pinned_get(ctx, sizeof(double) * ((size_t)nup * r + s + 8));
+  double* hres = (double*)pinned_get(ctx, sizeof(double) * ((size_t)nup * r + 2 * s + 8));
   if (!base || !partial || !hres) return set_err(ctx, KST_ERR_CUDA, "heig_top: workspace");
   cplx* Z = (cplx*)base;
   cplx* Y = Z + nb;
@@ -971,10 +971,11 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   cplx* X = Zn + nb;
   cplx* Cm = X + nb;
   cplx* Qm = Cm + s * s;
-  double* theta = (double*)(Qm + s * s);
+  // [residual partials | theta | vout | info] contiguous: one readback per iteration
+  double* res_part = (double*)(Qm + s * s);
+  double* theta = res_part + (size_t)nup * r;
   double* vout = theta + s;
   int* info = (int*)(vout + s);
-  double* res_part = (double*)(partial + (size_t)nblk * 2 * s * s);
   const size_t small_smem = ((jac_smem_bytes(s) + 15) / 16) * 16 + sizeof(cplx) * 4 * s * s;
   static bool small_attr = false;
   if (!small_attr) {
@@ -1025,15 +1026,13 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
     cplx* Zcur = Z;
     KST_TRY(step(Zcur, Y, Y2, 0));  // X = Ritz vectors of span(Zcur); Z <- orth(B^2 Zcur)
-    KST_CUDA(ctx, cudaMemcpyAsync(hres, res_part, sizeof(double) * nup * r, cudaMemcpyDeviceToHost, st));
-    KST_CUDA(ctx, cudaMemcpyAsync(hres + (size_t)nup * r, theta, sizeof(double) * s,
-                                  cudaMemcpyDeviceToHost, st));
-    KST_CUDA(ctx, cudaMemcpyAsync((int*)(hres + (size_t)nup * r + s), info, 2 * sizeof(int),
+    KST_CUDA(ctx, cudaMemcpyAsync(hres, res_part,
+                                  sizeof(double) * ((size_t)nup * r + 2 * s) + 2 * sizeof(int),
                                   cudaMemcpyDeviceToHost, st));
     KST_CUDA(ctx, cudaStreamSynchronize(st));
     const double* th = hres + (size_t)nup * r;
-    const int kept = *(int*)(hres + (size_t)nup * r + s);
-    const int path = *((int*)(hres + (size_t)nup * r + s) + 1);
+    const int kept = *(int*)(hres + (size_t)nup * r + 2 * s);
+    const int path = *((int*)(hres + (size_t)nup * r + 2 * s) + 1);
     double tmax = 0.0, worst = 0.0;
     for (int k = 0; k < s; ++k) tmax = std::max(tmax, std::fabs(th[k]));
     // Converged when every wanted Ritz pair has residual <= 1e-12 max|theta|

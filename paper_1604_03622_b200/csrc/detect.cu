@@ -19,6 +19,7 @@
 // Multipass (`pass_images`, src/multipass.py:83-102) filters once and
 // emits one map per row block of the stacked grid (`groups`).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -641,6 +642,336 @@ __global__ void __launch_bounds__(NT) filter_apply_kernel(
     if (i < P) out[(m * P + i) * q + t] = y[i];
 }
 
+#define KST_DISPATCH_P4(P, ...)                           \
+  switch (P) {                                            \
+    case 1: { constexpr int PP = 1; __VA_ARGS__; } break; \
+    case 2: { constexpr int PP = 2; __VA_ARGS__; } break; \
+    case 3: { constexpr int PP = 3; __VA_ARGS__; } break; \
+    default: { constexpr int PP = 4; __VA_ARGS__; } break; \
+  }
+
+// ---------------------------------------------------------------- fused per-bin detection
+// Uniform Doppler grid, q <= D, P <= 4, radices in {2, 3, 4, 5, 7, 11, 13, 23,
+// 29}: persistent CTAs (one per SM) walk the range bins. A bin's P channel
+// rows are staged in smem by bulk async copies (the next bin's rows are
+// prefetched into the free ping-pong buffer while this bin's pixels are
+// formed), transformed together by a multi-row Stockham FFT (every stage
+// has P x more independent butterflies than a one-row CTA), the temporal
+// coefficients come from Parseval on the spectra,
+//   c_ik = sum_t x_i[t] conj(U_B[t,k]) = (1/D) sum_d X_i[d] conj(U^_k[d])
+// (exact identity for the zero-padded length-D transform), and the per-pixel
+// projection, spatial candidates and max run straight from smem: the spectra
+// never round-trip through HBM and one launch replaces two.
+#ifndef KST_FB_NT
+#define KST_FB_NT 512
+#endif
+constexpr int FB_NT = KST_FB_NT;
+constexpr int FB_MAXP = 4;
+constexpr int FB_MAXKB = 4;
+constexpr int FB_MAXG = 64;
+
+struct FusedArgs {
+  int P, q, D, ka, kb, G, groups, mode, spatial;
+  double inv_sqrt_q, inv_D;
+};
+
+// radix-R Stockham stage over P rows (row stride D): small radices in registers
+template <int R>
+__device__ __forceinline__ void mr_stage_small(const cplx* __restrict__ a, cplx* __restrict__ b,
+                                               const cplx* __restrict__ w, int D, int Ns, int P) {
+  const int DR = D / R, step = D / (Ns * R);
+  for (int it = threadIdx.x; it < P * DR; it += FB_NT) {
+    const int row = it / DR, j = it - row * DR;
+    const cplx* ar = a + (size_t)row * D;
+    cplx* br = b + (size_t)row * D;
+    const int k = j % Ns, dst = (j / Ns) * Ns * R + k;
+    cplx t[R];
+    t[0] = ar[j];
+#pragma unroll
+    for (int r = 1; r < R; ++r) t[r] = cmul(ar[j + r * DR], w[r * k * step]);
+    if (R == 2) {
+      br[dst] = cadd(t[0], t[1]);
+      br[dst + Ns] = csub(t[0], t[1]);
+    } else if (R == 4) {
+      const cplx s02 = cadd(t[0], t[2]), d02 = csub(t[0], t[2]);
+      const cplx s13 = cadd(t[1], t[3]), d13 = csub(t[1], t[3]);
+      br[dst] = cadd(s02, s13);
+      br[dst + Ns] = cmk(d02.x + d13.y, d02.y - d13.x);
+      br[dst + 2 * Ns] = csub(s02, s13);
+      br[dst + 3 * Ns] = cmk(d02.x - d13.y, d02.y + d13.x);
+    } else {
+      constexpr int h = (R - 1) / 2, off = rtw_off(R);
+#pragma unroll
+      for (int r = 1; r <= h; ++r) {
+        const cplx sr = cadd(t[r], t[R - r]), dr = csub(t[r], t[R - r]);
+        t[r] = sr;
+        t[R - r] = dr;
+      }
+      cplx x0 = t[0];
+#pragma unroll
+      for (int r = 1; r <= h; ++r) x0 = cadd(x0, t[r]);
+      br[dst] = x0;
+#pragma unroll
+      for (int u = 1; u <= h; ++u) {
+        double ax = t[0].x, ay = t[0].y, bx = 0.0, by = 0.0;
+#pragma unroll
+        for (int r = 1; r <= h; ++r) {
+          const int m = (r * u) % R;
+          const double wc = c_plan.rtw[2 * (off + m)], ws = c_plan.rtw[2 * (off + m) + 1];
+          ax = fma(wc, t[r].x, ax);
+          ay = fma(wc, t[r].y, ay);
+          bx = fma(-ws, t[R - r].x, bx);
+          by = fma(-ws, t[R - r].y, by);
+        }
+        br[dst + u * Ns] = cmk(ax + by, ay - bx);
+        br[dst + (R - u) * Ns] = cmk(ax - by, ay + bx);
+      }
+    }
+  }
+}
+
+// large odd radix over P rows: phase A (twiddled pairs in place, X_0 out),
+// barrier, phase B (grouped output pairs, grp_unit per row)
+template <int R, int GU>
+__device__ void mr_stage_grp(cplx* __restrict__ a, cplx* __restrict__ b, const cplx* __restrict__ w,
+                             int D, int Ns, int P) {
+  constexpr int h = (R - 1) / 2, NGR = (h + GU - 1) / GU;
+  const int DR = D / R, step = D / (Ns * R);
+  for (int it = threadIdx.x; it < P * DR; it += FB_NT) {
+    const int row = it / DR, j = it - row * DR;
+    cplx* ar = a + (size_t)row * D;
+    const int k = j % Ns, dst = (j / Ns) * Ns * R + k;
+    cplx x0 = ar[j];
+#pragma unroll
+    for (int r = 1; r <= h; ++r) {
+      const cplx tr = cmul(ar[j + r * DR], w[r * k * step]);
+      const cplx tm = cmul(ar[j + (R - r) * DR], w[(R - r) * k * step]);
+      const cplx sr = cadd(tr, tm);
+      ar[j + r * DR] = sr;
+      ar[j + (R - r) * DR] = csub(tr, tm);
+      x0 = cadd(x0, sr);
+    }
+    b[(size_t)row * D + dst] = x0;
+  }
+  __syncthreads();
+  for (int un = threadIdx.x; un < P * DR * NGR; un += FB_NT) {
+    const int g = un / (P * DR), it = un - g * (P * DR);
+    const int row = it / DR, j = it - row * DR;
+    const cplx* ar = a + (size_t)row * D;
+    cplx* br = b + (size_t)row * D;
+    if (g == 0) grp_unit<R, GU, 0>(ar, br, j, DR, Ns);
+    if (NGR > 1 && g == 1) grp_unit<R, GU, (NGR > 1 ? 1 : 0)>(ar, br, j, DR, Ns);
+    if (NGR > 2 && g == 2) grp_unit<R, GU, (NGR > 2 ? 2 : 0)>(ar, br, j, DR, Ns);
+  }
+}
+
+// P-row Stockham FFT, a -> (a or b); returns the buffer holding the spectra
+__device__ cplx* mr_fft(cplx* a, cplx* b, const cplx* __restrict__ w, int D, int P) {
+  int Ns = 1;
+  for (int f = 0; f < c_plan.nf; ++f) {
+    const int R = c_plan.radix[f];
+    switch (R) {
+      case 2: mr_stage_small<2>(a, b, w, D, Ns, P); break;
+      case 3: mr_stage_small<3>(a, b, w, D, Ns, P); break;
+      case 4: mr_stage_small<4>(a, b, w, D, Ns, P); break;
+      case 5: mr_stage_small<5>(a, b, w, D, Ns, P); break;
+      case 7: mr_stage_small<7>(a, b, w, D, Ns, P); break;
+      case 11: mr_stage_grp<11, 5>(a, b, w, D, Ns, P); break;
+      case 13: mr_stage_grp<13, 6>(a, b, w, D, Ns, P); break;
+      case 23: mr_stage_grp<23, 4>(a, b, w, D, Ns, P); break;
+      default: mr_stage_grp<29, 7>(a, b, w, D, Ns, P); break;
+    }
+    __syncthreads();
+    cplx* t = a;
+    a = b;
+    b = t;
+    Ns *= R;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void fb_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t ad = (uint32_t)__cvta_generic_to_shared(bar);
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(ad), "r"(parity)
+        : "memory");
+}
+// one thread: bulk-copy bin m's P rows (q entries each) to rows of length D at dst
+__device__ __forceinline__ void fb_issue(const cplx* __restrict__ cube, int64_t m, int P, int q,
+                                         int D, cplx* dst, uint64_t* bar) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+               "r"((uint32_t)(P * q * sizeof(cplx)))
+               : "memory");
+  for (int i = 0; i < P; ++i)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(dst + (size_t)i * D)),
+        "l"(cube + (m * P + i) * q), "r"((uint32_t)(q * sizeof(cplx))), "r"(b)
+        : "memory");
+}
+
+template <int PT>
+__global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
+    const cplx* __restrict__ cube, int64_t n, const cplx* __restrict__ w,
+    const cplx* __restrict__ ubspec, const cplx* __restrict__ ua, const cplx* __restrict__ hconj,
+    FusedArgs fa, double* __restrict__ values, int* __restrict__ nonfinite) {
+  constexpr int P = PT, NC = P * FB_MAXKB;
+  extern __shared__ __align__(128) unsigned char fb_smem[];
+  const int D = fa.D, q = fa.q;
+  cplx* buf0 = (cplx*)fb_smem;
+  cplx* buf1 = buf0 + (size_t)P * D;
+  __shared__ cplx s_ua[FB_MAXP * FB_MAXP];
+  __shared__ cplx s_c[NC], s_e[NC];
+  __shared__ cplx s_h[FB_MAXG * FB_MAXP];
+  __shared__ double red[FB_NT / 32][2 * NC];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < P * fa.ka; e += FB_NT) s_ua[e] = ua[e];
+  for (int e = tid; e < fa.G * P; e += FB_NT) s_h[e] = hconj[e];
+  if (tid == 0) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < n) fb_issue(cube, blockIdx.x, P, q, D, buf0, &bar);
+  }
+  cplx* in = buf0;
+  cplx* other = buf1;
+  uint32_t phase = 0;
+  const int per = fa.G / fa.groups;
+  for (int64_t m = blockIdx.x; m < n; m += gridDim.x, phase ^= 1u) {
+    // zero padding [q, D) of the input rows (the FFT overwrote it last bin)
+    for (int e = tid; e < P * (D - q); e += FB_NT) {
+      const int i = e / (D - q), t = q + e % (D - q);
+      in[(size_t)i * D + t] = cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    fb_mbar_wait(&bar, phase);
+    if (nonfinite) {
+      int bad = 0;
+      for (int e = tid; e < P * q; e += FB_NT) {
+        const cplx v = in[(size_t)(e / q) * D + e % q];
+        if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+      }
+      if (bad) atomicOr(nonfinite, 1);
+    }
+    cplx* X = mr_fft(in, other, w, D, P);
+    cplx* fr = (X == in) ? other : in;  // free buffer: prefetch the next bin
+    if (tid == 0 && m + gridDim.x < n) fb_issue(cube, m + gridDim.x, P, q, D, fr, &bar);
+    // coefficients by Parseval (fixed-order reduction: deterministic)
+    if (fa.mode != 2) {
+      double acc[2 * NC];
+#pragma unroll
+      for (int c = 0; c < 2 * NC; ++c) acc[c] = 0.0;
+      for (int d = tid; d < D; d += FB_NT) {
+#pragma unroll
+        for (int k = 0; k < FB_MAXKB; ++k) {
+          if (k < fa.kb) {
+            const cplx u = __ldcg(&ubspec[(int64_t)k * D + d]);  // L2 only: L1 keeps the twiddles
+#pragma unroll
+            for (int i = 0; i < P; ++i) {
+              cplx c = cmk(acc[2 * (i * FB_MAXKB + k)], acc[2 * (i * FB_MAXKB + k) + 1]);
+              cfmac(c, X[(size_t)i * D + d], u);
+              acc[2 * (i * FB_MAXKB + k)] = c.x;
+              acc[2 * (i * FB_MAXKB + k) + 1] = c.y;
+            }
+          }
+        }
+      }
+      const int wid = tid >> 5, lane = tid & 31;
+#pragma unroll
+      for (int c = 0; c < 2 * NC; ++c) {
+        double v = acc[c];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[wid][c] = v;
+      }
+      __syncthreads();
+      if (tid < P * fa.kb) {
+        const int i = tid / fa.kb, k = tid % fa.kb;
+        double re = 0.0, im = 0.0;
+        for (int w2 = 0; w2 < FB_NT / 32; ++w2) {
+          re += red[w2][2 * (i * FB_MAXKB + k)];
+          im += red[w2][2 * (i * FB_MAXKB + k) + 1];
+        }
+        s_c[i * fa.kb + k] = cmk(re * fa.inv_D, im * fa.inv_D);
+      }
+      __syncthreads();
+      if (fa.mode == 1) {  // classical: E = U_A (U_A^H c)  (src/filters.py:115-116)
+        if (tid < P * fa.kb) {
+          const int i = tid / fa.kb, k = tid % fa.kb;
+          cplx acc2 = cmk(0, 0);
+          for (int al = 0; al < fa.ka; ++al) {
+            cplx inner = cmk(0, 0);
+            for (int j = 0; j < P; ++j) cfmca(inner, s_ua[j * fa.ka + al], s_c[j * fa.kb + k]);
+            cfma(acc2, s_ua[i * fa.ka + al], inner);
+          }
+          s_e[tid] = acc2;
+        }
+        __syncthreads();
+        if (tid < P * fa.kb) s_c[tid] = s_e[tid];
+        __syncthreads();
+      }
+    }
+    // per pixel: projection, spatial candidates, max |z|
+    for (int d = tid; d < D; d += FB_NT) {
+      cplx y[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) y[i] = X[(size_t)i * D + d];
+      if (fa.mode != 2) {
+        for (int k = 0; k < fa.kb; ++k) {
+          const cplx u = __ldcg(&ubspec[(int64_t)k * D + d]);  // L2 only: L1 keeps the twiddles
+#pragma unroll
+          for (int i = 0; i < P; ++i) y[i] = csub(y[i], cmul(s_c[i * fa.kb + k], u));
+        }
+      }
+      if (fa.spatial) {
+        for (int al = 0; al < fa.ka; ++al) {
+          cplx alpha = cmk(0, 0);
+#pragma unroll
+          for (int i = 0; i < P; ++i) cfmca(alpha, s_ua[i * fa.ka + al], y[i]);
+#pragma unroll
+          for (int i = 0; i < P; ++i) y[i] = csub(y[i], cmul(s_ua[i * fa.ka + al], alpha));
+        }
+      }
+      for (int gr = 0; gr < fa.groups; ++gr) {
+        double best2 = -1.0;
+        cplx zb = cmk(0, 0);
+        for (int g = gr * per; g < (gr + 1) * per; ++g) {
+          cplx z = cmk(0, 0);
+#pragma unroll
+          for (int i = 0; i < P; ++i) cfma(z, s_h[g * P + i], y[i]);
+          const double m2 = cabs2(z);
+          if (m2 > best2) {
+            best2 = m2;
+            zb = z;
+          }
+        }
+        values[((int64_t)gr * n + m) * D + d] = hypot(zb.x * fa.inv_sqrt_q, zb.y * fa.inv_sqrt_q);
+      }
+    }
+    __syncthreads();  // X and the coefficient smem are free for the next bin
+    in = fr;
+    other = X;
+  }
+}
+
+// host: can the fused kernel take this problem
+bool fused_ok(const Plan& plan, int P, int q, int D, int kb, int G) {
+  if (P > FB_MAXP || q > D || kb > FB_MAXKB || G > FB_MAXG) return false;
+  if ((size_t)2 * P * D * sizeof(cplx) > 200 * 1024) return false;
+  for (int f = 0; f < plan.nf; ++f) {
+    const int R = plan.radix[f];
+    if (R != 2 && R != 3 && R != 4 && R != 5 && R != 7 && R != 11 && R != 13 && R != 23 && R != 29)
+      return false;
+  }
+  return true;
+}
+
 // filter semantics -> (mode, spatial) (src/filters.py:98-116)
 // mode 0: temporal projection coefficients, 1: joint (classical), 2: none
 void filter_mode(int kind, bool has_a, bool has_b, int spatial_only, int& mode, int& spatial) {
@@ -709,17 +1040,23 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
     return set_err(ctx, KST_ERR_DIMENSION, "detect: q=%d too long for the direct-sum path", q);
 
   const int64_t rows = n * p;
-  // workspace: spec (rows x D), coef (rows x kb), ubspec (kb x D), ubT (kb x q),
-  // twiddles (D), hconj (G x p), dop (D), flag
-  const size_t bytes = sizeof(cplx) * ((size_t)rows * D + (size_t)rows * std::max(kb_used, 1) +
+  // fused per-bin kernel (no spectra in HBM) when the plan fits it
+  FusedArgs fa;
+  static const bool fused_on = !(getenv("KST_DET_FUSED") && atoi(getenv("KST_DET_FUSED")) == 0);
+  const bool fused = uniform && fused_on && fused_ok(plan, p, q, D, kb_used, G);
+  const int64_t srows = fused ? 0 : rows;  // spectra / coefficient rows in HBM
+  // workspace: spec (srows x D), coef (srows x kb), ubspec (kb x D), ubT (kb x q),
+  // twiddles (D), hconj (G x p), dop (D), flag (2), perm (D)
+  const size_t bytes = sizeof(cplx) * ((size_t)srows * D + (size_t)srows * std::max(kb_used, 1) +
                                        (size_t)std::max(kb_used, 1) * (D + q) + D + (size_t)G * p) +
-                       sizeof(double) * D + 256;
+                       sizeof(double) * D + sizeof(int) * (D + 4) + 256;
   char* base = (char*)ws_get(ctx, WS_DET, bytes);
-  cplx* hstage = (cplx*)pinned_get(ctx, sizeof(cplx) * (size_t)G * p + sizeof(double) * D + 64);
+  cplx* hstage = (cplx*)pinned_get(ctx, sizeof(cplx) * (size_t)G * p + sizeof(double) * D +
+                                            sizeof(int) * D + 64);
   if (!base || !hstage) return set_err(ctx, KST_ERR_CUDA, "detect: workspace");
   cplx* spec = (cplx*)base;
-  cplx* coef = spec + (size_t)rows * D;
-  cplx* ubspec = coef + (size_t)rows * std::max(kb_used, 1);
+  cplx* coef = spec + (size_t)srows * D;
+  cplx* ubspec = coef + (size_t)srows * std::max(kb_used, 1);
   cplx* ubT = ubspec + (size_t)std::max(kb_used, 1) * D;
   cplx* tw = ubT + (size_t)std::max(kb_used, 1) * q;
   cplx* hconj = tw + D;
@@ -731,7 +1068,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   std::vector<double> key;
   key.reserve(8 + D + 2 * (size_t)G * p);
   for (double v : {(double)D, (double)G, (double)p, (double)q, (double)kb_used, (double)uniform,
-                   (double)rows})
+                   (double)srows, (double)fused})
     key.push_back(v);
   key.insert(key.end(), dop_host, dop_host + D);
   key.insert(key.end(), (const double*)grid_host, (const double*)grid_host + 2 * (size_t)G * p);
@@ -767,6 +1104,38 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
                                                    ubspec, nullptr, flag + 1);
     KST_LAUNCH(ctx);
   }
+  if (fused) {
+    fa.P = p;
+    fa.q = q;
+    fa.D = D;
+    fa.ka = has_a ? ka : 0;
+    fa.kb = kb_used;
+    fa.G = G;
+    fa.groups = groups;
+    fa.mode = mode;
+    fa.spatial = spatial;
+    fa.inv_sqrt_q = 1.0 / sqrt((double)q);
+    fa.inv_D = 1.0 / (double)D;
+    const int fsm = (int)(2 * sizeof(cplx) * p * D);
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    KST_DISPATCH_P4(p, {
+      static bool attr = false;
+      if (!attr) {
+        KST_CUDA(ctx, cudaFuncSetAttribute(detect_bin_kernel<PP>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+      }
+      detect_bin_kernel<PP><<<(unsigned)std::min<int64_t>(n, nsm), FB_NT, fsm, st>>>(
+          cube, n, tw, ubspec, has_a ? ua : hconj, hconj, fa, values,
+          check_finite ? flag : nullptr);
+    });
+    KST_LAUNCH(ctx);
+  } else {
   row_spectrum_kernel<<<(unsigned)rows, NTS, smem, st>>>(cube, rows, q, ub, kb_used, tw, D, uniform,
                                                         dop, spec, coef,
                                                         check_finite ? flag : nullptr);
@@ -785,6 +1154,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
                                           sizeof(cplx) * G * p, st>>>(
                         spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n)));
   KST_LAUNCH(ctx);
+  }
   if (!check_finite) return KST_OK;
   int hflag = 0;
   KST_CUDA(ctx, cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -673,7 +673,31 @@ constexpr int FB_MAXG = 64;
 struct FusedArgs {
   int P, q, D, ka, kb, G, groups, mode, spatial;
   double inv_sqrt_q, inv_D;
+  // dft = 1: the spatial grid is make_spatial_grid(P, G) (src/filters.py:208-217)
+  // with G % 4 == 0, so z_g = (1/sqrt P) sum_i y_i W^{g i}, W = e^{-2 pi i/G},
+  // splits as g = g0 + (G/4) g1 into twiddles W^{g0 i} and a 4-point DFT over
+  // i; w4[g0][i] = W^{g0 i}, scale = 1/sqrt(P q)
+  int dft;
+  double scale;
+  double w4[FB_MAXG / 4][FB_MAXP][2];
 };
+
+// sums v[0..31] over the warp; lane l returns the warp total of value l
+// (transposing butterfly: 31 exchanges instead of 32 x 5)
+__device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int j = 0; j < o; ++j) {
+      const double send = up ? v[j] : v[j + o];
+      const double keep = up ? v[j + o] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0];
+}
 
 // radix-R Stockham stage over P rows (row stride D): small radices in registers
 template <int R>
@@ -829,11 +853,14 @@ __global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
   __shared__ cplx s_ua[FB_MAXP * FB_MAXP];
   __shared__ cplx s_c[NC], s_e[NC];
   __shared__ cplx s_h[FB_MAXG * FB_MAXP];
+  __shared__ cplx s_w4[FB_MAXG / 4 * FB_MAXP];
   __shared__ double red[FB_NT / 32][2 * NC];
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   for (int e = tid; e < P * fa.ka; e += FB_NT) s_ua[e] = ua[e];
   for (int e = tid; e < fa.G * P; e += FB_NT) s_h[e] = hconj[e];
+  for (int e = tid; e < FB_MAXG / 4 * FB_MAXP; e += FB_NT)
+    s_w4[e] = cmk(fa.w4[e / FB_MAXP][e % FB_MAXP][0], fa.w4[e / FB_MAXP][e % FB_MAXP][1]);
   if (tid == 0) {
     const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
@@ -884,11 +911,12 @@ __global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
         }
       }
       const int wid = tid >> 5, lane = tid & 31;
+      {
+        double v[32];
 #pragma unroll
-      for (int c = 0; c < 2 * NC; ++c) {
-        double v = acc[c];
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) red[wid][c] = v;
+        for (int c = 0; c < 32; ++c) v[c] = (c < 2 * NC) ? acc[c] : 0.0;
+        const double tot = warp_transpose_reduce32(v);
+        if (lane < 2 * NC) red[wid][lane] = tot;
       }
       __syncthreads();
       if (tid < P * fa.kb) {
@@ -938,6 +966,32 @@ __global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
           for (int i = 0; i < P; ++i) y[i] = csub(y[i], cmul(s_ua[i * fa.ka + al], alpha));
         }
       }
+      if (fa.dft) {
+        // max_g |z_g|^2 via g = g0 + (G/4) g1: t_i = y_i W^{g0 i}, then the
+        // 4-point DFT over i in pairs, max(|a + c|^2, |a - c|^2) =
+        // |a|^2 + |c|^2 + 2 |Re(a conj c)| (a = t0 + t2, c = t1 + t3) and
+        // max(|b - ie|^2, |b + ie|^2) = |b|^2 + |e|^2 + 2 |Im(b conj e)|
+        double best2 = 0.0;
+        const int G4 = fa.G >> 2;
+        for (int g0 = 0; g0 < G4; ++g0) {
+          cplx t[4];
+          t[0] = y[0];
+#pragma unroll
+          for (int i = 1; i < 4; ++i)
+            t[i] = (i < P) ? cmul(y[i], s_w4[g0 * FB_MAXP + i]) : cmk(0.0, 0.0);
+          const cplx a = cadd(t[0], t[2]), b = csub(t[0], t[2]);
+          const cplx c = (P > 3) ? cadd(t[1], t[3]) : t[1];
+          const cplx e = (P > 3) ? csub(t[1], t[3]) : t[1];
+          const double aa = fma(a.x, a.x, a.y * a.y), bb = fma(b.x, b.x, b.y * b.y);
+          const double cc = fma(c.x, c.x, c.y * c.y);
+          const double ee = (P > 3) ? fma(e.x, e.x, e.y * e.y) : cc;
+          const double re = fma(a.x, c.x, a.y * c.y), im = fma(b.y, e.x, -b.x * e.y);
+          best2 = fmax(best2, fma(2.0, fabs(re), aa + cc));
+          best2 = fmax(best2, fma(2.0, fabs(im), bb + ee));
+        }
+        values[m * D + d] = sqrt(best2) * fa.scale;
+        continue;
+      }
       for (int gr = 0; gr < fa.groups; ++gr) {
         double best2 = -1.0;
         cplx zb = cmk(0, 0);
@@ -958,6 +1012,21 @@ __global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
     in = fr;
     other = X;
   }
+}
+
+// host: is grid[g, i] = exp(2 pi i (g / G) i) / sqrt(p) (make_spatial_grid,
+// src/filters.py:208-217) to within rounding
+bool dft_grid(const cplx* grid, int G, int p) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  const long double s = 1.0L / sqrtl((long double)p);
+  for (int g = 0; g < G; ++g)
+    for (int i = 0; i < p; ++i) {
+      const long double th = 2.0L * pi * ((long double)g / G) * i;
+      const long double dx = (long double)grid[g * p + i].x - s * cosl(th);
+      const long double dy = (long double)grid[g * p + i].y - s * sinl(th);
+      if (fabsl(dx) > 4e-16L || fabsl(dy) > 4e-16L) return false;
+    }
+  return true;
 }
 
 // host: can the fused kernel take this problem
@@ -1116,6 +1185,15 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
     fa.spatial = spatial;
     fa.inv_sqrt_q = 1.0 / sqrt((double)q);
     fa.inv_D = 1.0 / (double)D;
+    fa.dft = (groups == 1 && G % 4 == 0 && dft_grid(grid_host, G, p)) ? 1 : 0;
+    fa.scale = 1.0 / sqrt((double)p * (double)q);
+    for (int g0 = 0; g0 < FB_MAXG / 4; ++g0)
+      for (int i = 0; i < FB_MAXP; ++i) {
+        const long double th =
+            -2.0L * 3.141592653589793238462643383279502884L * (long double)(g0 * i) / (long double)G;
+        fa.w4[g0][i][0] = (double)cosl(th);
+        fa.w4[g0][i][1] = (double)sinl(th);
+      }
     const int fsm = (int)(2 * sizeof(cplx) * p * D);
     static int nsm = 0;
     if (!nsm) {

@@ -153,6 +153,22 @@ int kst_filter(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
                const double* ua, int ka, const double* ub, int kb, int kind,
                int spatial_only, double* out, void* stream);
 
+/*
+ * "optimal" filter.
+ * kst_chol replaces build_filter(kind="optimal") (src/filters.py:144-163:
+ *   as_matrix finite check, then scipy cho_factor(sigma, lower=True)):
+ *   sigma dev (d, d) complex row-major, only its lower triangle is read;
+ *   L dev (d, d) complex receives the column-major lower Cholesky factor.
+ *   KST_ERR_DATA if sigma has a non-finite entry or is not positive definite.
+ * kst_chol_solve replaces StapFilter.apply_matrix for kind "optimal"
+ *   (src/filters.py:98-100: cho_solve): X = sigma^-1 B for every column of the
+ *   column-major (d, nrhs) matrix B, i.e. every bin of an (nrhs, p, q) cube
+ *   with d = p q. X may equal B. KST_ERR_DATA if B has a non-finite entry.
+ */
+int kst_chol(kst_ctx* ctx, const double* sigma, int d, double* L, void* stream);
+int kst_chol_solve(kst_ctx* ctx, const double* L, int d, const double* B,
+                   int64_t nrhs, double* X, void* stream);
+
 /* change_detect (src/multipass.py:105-123): out = |a - b| (or a - b). */
 int kst_change(kst_ctx* ctx, const double* a, const double* b, int64_t count,
                int is_signed, double* out, void* stream);

@@ -251,6 +251,40 @@ def multipass_cases():
     np.savez_compressed(os.path.join(OUT, "multipass_cases.npz"), **out)
 
 
+def optimal_cases():
+    """kind "optimal" (src/filters.py:144-163, 98-100), steering, filter_output
+    and SINR (src/filters.py:44-55, 178-198) on seeded scenes: the whitened
+    detection map against the scene's true covariance, and the SINR of the
+    kron / classical / optimal weights (acceptance criteria 6/7 shape)."""
+    ks, filters, lrkron, multipass, simulate, c2s = _ref()
+    out = {}
+    cfg = simulate.SceneConfig(p=3, q=32, n_bins=48, rank_temporal=4, noise_power=1e-2, seed=1000)
+    sigma = simulate.scene_model(cfg).total_covariance()
+    hist = simulate.inject_target(simulate.gen_clutter(cfg), 9, 0.25, 3.0)
+    cube = hist.data[0]
+    filt = filters.build_filter("optimal", sigma=sigma, p=3, q=32)
+    dop, grid = filters.make_doppler_grid(32), filters.make_spatial_grid(3, 8)
+    out["sigma"] = sigma
+    out["cube"] = cube
+    out["whitened"] = np.stack([filt.apply_matrix(cube[m]) for m in range(cube.shape[0])])
+    out["map"] = filters.detection_image(filt, cube, dop, grid).values
+    est = lrkron.lr_kron_estimate(lrkron.sample_covariance(c2s(cube[:5]), 3, 32), 1, 4)
+    sv = filters.make_steering(0.25, 3, 32, kappa=2.0)
+    out["steering"] = sv.vector
+    vals, outs = [], []
+    for kind in ("kron", "classical"):
+        f = filters.build_filter(kind, estimate=est)
+        vals.append(filters.sinr(f.apply(sv.vector), sv, 2.0, sigma))
+        outs.append(filters.filter_output(f, sv, cube[9].ravel()))
+    vals.append(filters.sinr(filt.apply(sv.vector), sv, 2.0, sigma))
+    outs.append(filters.filter_output(filt, sv, cube[9].ravel()))
+    out["sinr"] = np.array(vals)
+    out["filter_output"] = np.array(outs)
+    out["est_spatial"] = est.spatial
+    out["est_temporal"] = est.temporal
+    np.savez_compressed(os.path.join(OUT, "optimal_cases.npz"), **out)
+
+
 def scene_hashes():
     """SHA-256 of reference-simulated cubes; pins scenes.py bit-exactly."""
     ks, filters, lrkron, multipass, simulate, c2s = _ref()
@@ -293,6 +327,7 @@ def main():
     eig_cases()
     detect_cases()
     multipass_cases()
+    optimal_cases()
     scene_hashes()
 
 

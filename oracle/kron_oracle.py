@@ -279,6 +279,35 @@ def detect(kind, ua, ub, cube, dopplers, grid, spatial_only=False):
 
 
 # --------------------------------------------------------------------------
+# "optimal" kind, steering, SINR -- src/filters.py:27-55, 98-100, 144-163, 178-198
+
+
+def optimal_whiten(sigma, cube):
+    """sigma^-1 x per bin: cho_factor(sigma, lower=True) (src/filters.py:156-162)
+    then cho_solve per bin (src/filters.py:98-100); all bins as one solve."""
+    from scipy.linalg import cho_factor, cho_solve
+    c = cho_factor(np.asarray(sigma, dtype=np.complex128), lower=True)
+    cube = np.asarray(cube, dtype=np.complex128)
+    n, p, q = cube.shape
+    return np.ascontiguousarray(cho_solve(c, cube.reshape(n, p * q).T).T).reshape(n, p, q)
+
+
+def steering(doppler, p, q, kappa=0.5):
+    """Unit-norm kron(spatial, temporal) steering snapshot (src/filters.py:38-55)."""
+    sp = np.exp(2j * np.pi * kappa * doppler * np.arange(p))
+    tm = np.exp(2j * np.pi * doppler * np.arange(q)) / np.sqrt(q)
+    full = np.kron(sp, tm)
+    return full / np.linalg.norm(full)
+
+
+def sinr(w, d, amplitude, sigma):
+    """|a|^2 |w^H d|^2 / (w^H sigma w) (src/filters.py:185-198)."""
+    w, d = np.asarray(w).ravel(), np.asarray(d).ravel()
+    denom = np.vdot(w, np.asarray(sigma) @ w).real
+    return float((abs(amplitude) ** 2) * abs(np.vdot(w, d)) ** 2 / denom)
+
+
+# --------------------------------------------------------------------------
 # multipass -- src/multipass.py
 
 

@@ -5,9 +5,10 @@ Mirrors `kronstap.filters` (src/filters.py) for the projection filters:
 `detection_image`, `DetectionMap` and the grids. Kernels: kst_subspace_basis
 (K3/K4), kst_detect (K5), kst_filter (whole-cube apply_matrix).
 
-Out of scope: the "optimal" (Cholesky-whitening) kind,
-steering / SINR helpers -- they are not on the image path. They raise
-NotImplementedError here instead of silently running on the CPU.
+The "optimal" (covariance-whitening) kind factors
+sigma once on the device (kst_chol) and whitens every bin with one solve
+(kst_chol_solve); steering vectors are host constructions like the grids,
+and filter_output / sinr evaluate on the device.
 """
 
 from __future__ import annotations
@@ -18,7 +19,7 @@ import numpy as np
 
 from . import _native as nat
 from ._dual import Dual
-from .errors import DimensionError
+from .errors import DataError, DimensionError
 from .linalg import subspace_basis_device
 
 FILTER_KINDS = ("optimal", "classical", "kron")
@@ -50,6 +51,7 @@ class StapFilter:
         self._ua = _basis_dual(spatial_basis)
         self._ub = _basis_dual(temporal_basis)
         self.spatial_only = spatial_only
+        self._chol = None  # kind "optimal": device (pq, pq) column-major lower factor
 
     @property
     def spatial_basis(self):
@@ -73,8 +75,6 @@ class StapFilter:
         return ua, ub
 
     def _kind_code(self):
-        if self.kind == "optimal":
-            raise NotImplementedError("the 'optimal' filter kind is out of scope for the GPU path")
         if self.kind not in nat.KIND:
             raise DimensionError(f"unknown filter kind {self.kind!r}")
         return nat.KIND[self.kind]
@@ -85,8 +85,11 @@ class StapFilter:
         shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
         if len(shp) != 3 or shp[1:] != (self.p, self.q):
             raise DimensionError(f"cube shape {shp} does not match filter ({self.p}, {self.q})")
-        kind = self._kind_code()
         x = nat.to_device(cube)
+        if self.kind == "optimal":
+            out = self._whiten(x)
+            return out if nat.is_device(cube) else nat.to_host(out)
+        kind = self._kind_code()
         ua, ub = self._dev_bases()
         out = torch.empty_like(x)
         c = nat.ctx(x.device)
@@ -95,6 +98,19 @@ class StapFilter:
             nat.ptr(ub), 0 if ub is None else ub.shape[1], kind, int(bool(self.spatial_only)),
             nat.ptr(out), nat.stream_of(x.device)), c)
         return out if nat.is_device(cube) else nat.to_host(out)
+
+    def _whiten(self, x):
+        """sigma^-1 applied to every bin of the device cube x (cho_solve,
+        src/filters.py:98-100): one kst_chol_solve over all bins."""
+        import torch
+        if self._chol is None:
+            raise DimensionError("optimal filter has no factor (use build_filter)")
+        L = self._chol if self._chol.device == x.device else self._chol.to(x.device)
+        out = torch.empty_like(x)
+        c = nat.ctx(x.device)
+        nat.check(nat.lib().kst_chol_solve(c, nat.ptr(L), self.p * self.q, nat.ptr(x), x.shape[0],
+                                           nat.ptr(out), nat.stream_of(x.device)), c)
+        return out
 
     def apply_matrix(self, x):
         """Filter one bin given as its (p, q) matrix (src/filters.py:88-116)."""
@@ -131,7 +147,7 @@ def build_filter(kind, estimate=None, sigma=None, p=None, q=None, drop_temporal=
     if kind not in FILTER_KINDS:
         raise DimensionError(f"unknown filter kind {kind!r}")
     if kind == "optimal":
-        raise NotImplementedError("the 'optimal' filter kind is out of scope for the GPU path")
+        return _optimal_filter(sigma, p, q)
     if estimate is None:
         raise DimensionError(f"{kind} filter needs a covariance estimate")
     device_mode = estimate._sp.device_mode if hasattr(estimate, "_sp") else nat.is_device(estimate.spatial)
@@ -156,6 +172,95 @@ def build_filter(kind, estimate=None, sigma=None, p=None, q=None, drop_temporal=
                    None if ub is None else Dual.from_device(ub, device_mode),
                    spatial_only=drop_temporal)
     return f
+
+
+def _optimal_filter(sigma, p, q):
+    """build_filter(kind="optimal") (src/filters.py:144-163): the lower Cholesky
+    factor of sigma on the device; DataError when sigma is non-finite or not
+    positive definite."""
+    import torch
+    if sigma is None or p is None or q is None:
+        raise DimensionError("optimal filter needs sigma and its bin shape")
+    shp = tuple(sigma.shape) if hasattr(sigma, "shape") else np.shape(sigma)
+    if len(shp) != 2:
+        raise DimensionError(f"covariance must be 2-D, got shape {shp}")
+    if shp != (p * q, p * q):
+        # as_matrix's finite check comes first in the reference (src/linalg.py:25-33)
+        host = sigma.cpu().numpy() if nat.is_device(sigma) else np.asarray(sigma)
+        if not np.all(np.isfinite(host)):
+            raise DataError("covariance contains non-finite entries")
+        raise DimensionError(f"covariance shape {shp} does not match p*q = {p * q}")
+    s = nat.to_device(sigma)
+    L = torch.empty_like(s)
+    c = nat.ctx(s.device)
+    nat.check(nat.lib().kst_chol(c, nat.ptr(s), p * q, nat.ptr(L), nat.stream_of(s.device)), c)
+    filt = StapFilter("optimal", p, q)
+    filt._chol = L
+    return filt
+
+
+@dataclass
+class SteeringVector:
+    """Spatial and temporal steering for one normalized Doppler (src/filters.py:27-41)."""
+
+    spatial: np.ndarray
+    temporal: np.ndarray
+    doppler: float
+    kappa: float
+
+    @property
+    def vector(self):
+        """Unit-norm channel-major steering snapshot."""
+        full = np.kron(self.spatial, self.temporal)
+        return full / np.linalg.norm(full)
+
+
+def make_steering(doppler, p, q, kappa=0.5):
+    """src/filters.py:44-55 (a host construction of p + q phase ramps, like the grids)."""
+    if p < 1 or q < 1:
+        raise DimensionError(f"steering needs positive dims, got p={p}, q={q}")
+    spatial = np.exp(2j * np.pi * kappa * doppler * np.arange(p))
+    temporal = np.exp(2j * np.pi * doppler * np.arange(q)) / np.sqrt(q)
+    return SteeringVector(spatial, temporal, float(doppler), float(kappa))
+
+
+def _dev_vector(v, dev):
+    import torch
+    if nat.is_device(v):
+        return v.reshape(-1).to(dev, torch.complex128)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.complex128).ravel())).to(dev)
+
+
+def filter_output(filt, steering, x):
+    """(F d)^H x for one snapshot (src/filters.py:178-182): F d through the
+    filter's device path, the inner product on the device."""
+    import torch
+    d = steering.vector if isinstance(steering, SteeringVector) else steering
+    dev = torch.device("cuda", torch.cuda.current_device())
+    w = _dev_vector(filt.apply(_dev_vector(d, dev)), dev)
+    return complex(torch.vdot(w, _dev_vector(x, dev)).item())
+
+
+def sinr(weights, steering, amplitude, sigma):
+    """Output SINR of a weight vector (src/filters.py:185-198), on the device:
+    |amplitude|^2 |w^H d|^2 / (w^H sigma w); scale invariant in w."""
+    import torch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    w = _dev_vector(weights, dev)
+    d = steering.vector if isinstance(steering, SteeringVector) else steering
+    d = _dev_vector(d, dev)
+    shp = tuple(sigma.shape) if hasattr(sigma, "shape") else np.shape(sigma)
+    if len(shp) != 2:
+        raise DimensionError(f"covariance must be 2-D, got shape {shp}")
+    s = nat.to_device(sigma) if nat.is_device(sigma) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(sigma, dtype=np.complex128))).to(dev)
+    if not bool(torch.isfinite(torch.view_as_real(s)).all()):
+        raise DataError("covariance contains non-finite entries")
+    denom = float(torch.vdot(w, s.to(dev) @ w).real.item())
+    if denom <= 0.0:
+        raise DataError("weights have no response power under this covariance")
+    num = (abs(amplitude) ** 2) * abs(complex(torch.vdot(w, d).item())) ** 2
+    return float(num / denom)
 
 
 def make_doppler_grid(count):
@@ -207,9 +312,13 @@ def run_detect(filt, cube, dop, grid, groups=1):
     shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
     if len(shp) != 3 or shp[1:] != (filt.p, filt.q):
         raise DimensionError(f"cube shape {shp} does not match filter ({filt.p}, {filt.q})")
-    kind = filt._kind_code()
     x = nat.to_device(cube)
-    ua, ub = filt._dev_bases()
+    if filt.kind == "optimal":
+        # whitened bins, then the identity projection (mode "kron", no bases)
+        x, kind, ua, ub = filt._whiten(x), nat.KIND["kron"], None, None
+    else:
+        kind = filt._kind_code()
+        ua, ub = filt._dev_bases()
     n, D, G = shp[0], dop.size, grid.shape[0]
     vals = torch.empty((groups, n, D), dtype=torch.float64, device=x.device)
     c = nat.ctx(x.device)

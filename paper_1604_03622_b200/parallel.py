@@ -68,3 +68,59 @@ def process_sequence(frames, rank_spatial=1, rank_temporal=3, dopplers=None, spa
         else torch.device("cpu")
     local = torch.stack([m.to(dev) for m in maps]) if maps else torch.zeros((0,), device=dev)
     return gather_maps(local, len(frames), group)
+
+
+# ----------------------------------------------------------------- L-mode tiles
+def tile_bounds(n_bins, world):
+    """Contiguous test-bin tiles [lo, hi) per rank, sizes differing by at most
+    one (windowed L-mode shards by bin tile + halo)."""
+    if n_bins < 0 or world < 1:
+        raise ValueError("n_bins >= 0 and world >= 1 required")
+    base, extra = divmod(n_bins, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def gather_tiles(local_rows, n_rows, group=None):
+    """All-gather row tiles (tile_bounds order) into the full (n_rows, ...) map
+    on every rank; tiles are padded to the largest tile for all_gather."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    bounds = tile_bounds(n_rows, world)
+    per = max(hi - lo for lo, hi in bounds)
+    k, *tail = local_rows.shape
+    assert k == bounds[rank][1] - bounds[rank][0]
+    pad = torch.zeros((per, *tail), dtype=local_rows.dtype, device=local_rows.device)
+    pad[:k] = local_rows
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([bufs[r][:hi - lo] for r, (lo, hi) in enumerate(bounds)])
+
+
+def windowed_sharded(cube, n_w, rank_spatial, rank_temporal, dopplers, spatial_grid, group=None,
+                     gather=True, **kw):
+    """L-mode detection of one frame tiled over the ranks of `group`: rank r
+    detects test bins tile_bounds(n_bins, W)[r], reading only its tile plus
+    the halo its training windows reach (windowed.halo_range); no exchange on
+    the data path. Returns the full (n_bins, D) map on every rank (gather) or
+    this rank's (hi - lo, D) tile."""
+    from .windowed import windowed_detection_image
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n_bins = int(cube.shape[0])
+    lo, hi = tile_bounds(n_bins, world)[rank]
+    if hi > lo:
+        vals = torch.as_tensor(windowed_detection_image(
+            cube, n_w, rank_spatial, rank_temporal, dopplers, spatial_grid, bins=(lo, hi),
+            **kw).values)
+    else:
+        vals = torch.zeros((0, len(dopplers)), dtype=torch.float64)
+    if not gather or world == 1:
+        return vals
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
+        else torch.device("cpu")
+    return gather_tiles(vals.to(dev), n_bins, group)

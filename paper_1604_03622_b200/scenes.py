@@ -98,6 +98,19 @@ def _model(cfg):
     return cal, prof, w
 
 
+def total_covariance(cfg):
+    """Exact snapshot covariance of a scene config: (h h^H) kron B + noise I
+    (SceneModel.total_covariance, src/simulate.py:93-105), the sigma that the
+    SINR acceptance criteria evaluate against (host ground truth, like the
+    simulator itself)."""
+    cal, prof, w = _model(cfg)
+    b = (prof * w) @ prof.conj().T
+    b = (b + b.conj().T) / 2.0
+    full = np.kron(np.outer(cal, cal.conj()), b)
+    full += cfg.noise_power * np.eye(full.shape[0])
+    return full
+
+
 def _texture(rng, cfg):
     if cfg.texture == "constant":
         return 1.0

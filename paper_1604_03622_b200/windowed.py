@@ -40,14 +40,26 @@ def window_bins(s, n_w, n_bins):
     return lo, hi
 
 
+def halo_range(lo, hi, n_w, n_bins):
+    """Bins [a, b) a tile of test bins [lo, hi) reads: its own bins plus the
+    halo its training windows reach (windowed L-mode)."""
+    if not 0 <= lo < hi <= n_bins:
+        raise DimensionError(f"test bins [{lo}, {hi}) outside [0, {n_bins})")
+    return window_start(lo, n_w, n_bins), window_start(hi - 1, n_w, n_bins) + n_w
+
+
 def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, spatial_grid,
                              kind="kron", tol=1e-4, max_iter=100, drop_temporal=False,
-                             return_estimates=False):
+                             return_estimates=False, bins=None):
     """Detection map of the windowed (L-mode) estimator; cube (n_bins, p, q).
 
     Returns a DetectionMap (host arrays for numpy input, device tensor values
     for CUDA input); with return_estimates=True also the list of
-    (window start, KronCovEstimate) pairs.
+    (window start, KronCovEstimate) pairs. bins=(lo, hi) computes only test
+    bins [lo, hi) (map rows lo..hi-1, shape (hi - lo, D)); a host cube then
+    has only the tile plus its halo (`halo_range`) copied to the device, so
+    a tile-sharded frame moves each bin to at most the GPUs whose windows
+    read it.
     """
     import torch
     shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
@@ -56,21 +68,24 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
     n_bins, p, q = shp
     if not 1 <= n_w <= n_bins:
         raise DimensionError(f"window n_w={n_w} must be in [1, {n_bins}]")
-    x = nat.to_device(cube)
+    lo, hi = (0, n_bins) if bins is None else (int(bins[0]), int(bins[1]))
+    a, b = halo_range(lo, hi, n_w, n_bins)
+    x = nat.to_device(cube[a:b])  # the tile and its halo; a view for CUDA input
     snaps = cube_to_snapshots(x)
     dev_out = nat.is_device(cube)
     D = int(np.asarray(dopplers.cpu() if nat.is_device(dopplers) else dopplers).size)
-    vals = torch.empty((n_bins, D), dtype=torch.float64, device=x.device)
+    vals = torch.empty((hi - lo, D), dtype=torch.float64, device=x.device)
     ests = []
     dop = grid = None
-    for s in range(n_bins - n_w + 1):
-        scm = sample_covariance(snaps[s:s + n_w], p, q)
+    for s in range(window_start(lo, n_w, n_bins), window_start(hi - 1, n_w, n_bins) + 1):
+        scm = sample_covariance(snaps[s - a:s - a + n_w], p, q)
         est = lr_kron_estimate(scm, rank_spatial, rank_temporal, tol=tol, max_iter=max_iter)
         filt = build_filter(kind, estimate=est, drop_temporal=drop_temporal)
         if dop is None:
             dop, grid = _host_grid_args(filt, dopplers, spatial_grid)
-        lo, hi = window_bins(s, n_w, n_bins)
-        vals[lo:hi] = run_detect(filt, x[lo:hi], dop, grid)[0]
+        t0, t1 = window_bins(s, n_w, n_bins)
+        t0, t1 = max(t0, lo), min(t1, hi)
+        vals[t0 - lo:t1 - lo] = run_detect(filt, x[t0 - a:t1 - a], dop, grid)[0]
         if return_estimates:
             ests.append((s, est))
     dmap = DetectionMap(vals if dev_out else nat.to_host(vals), dop, grid)

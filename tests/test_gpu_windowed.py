@@ -62,3 +62,26 @@ def test_windowed_device_tensors_stay_on_device():
     dmap = kst.windowed_detection_image(cube, 9, 1, 2, kst.make_doppler_grid(D),
                                         kst.make_spatial_grid(p, 16))
     assert dmap.values.is_cuda and tuple(dmap.values.shape) == (nb, D)
+
+
+@pytest.mark.parametrize("world,n_w", [(2, 9), (3, 25), (8, 9)])
+def test_bin_tiles_with_halo_equal_the_full_frame(world, n_w):
+    """SURVEY.md §8e windowed L-mode sharding: each tile (tile_bounds) reads
+    only its halo range; the tiles, concatenated, equal the one-GPU map
+    bitwise (host cube: only the halo range is uploaded; device cube: views)."""
+    from paper_1604_03622_b200 import parallel
+    from paper_1604_03622_b200.windowed import halo_range
+    p, q, nb, D, G = 3, 64, 40, 64, 16
+    cube = scenes.bench_scene(p, q, nb, seed=23, movers=4).data[0]
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    full = kst.windowed_detection_image(cube, n_w, 1, 3, dop, grid).values
+    tiles = []
+    for lo, hi in parallel.tile_bounds(nb, world):
+        a, b = halo_range(lo, hi, n_w, nb)
+        seen = np.full_like(cube, np.nan)  # bins outside the halo are never read
+        seen[a:b] = cube[a:b]
+        tiles.append(kst.windowed_detection_image(seen, n_w, 1, 3, dop, grid, bins=(lo, hi)).values)
+    assert np.array_equal(np.concatenate(tiles), full)
+    dev = torch.from_numpy(cube).cuda()
+    t1 = kst.windowed_detection_image(dev, n_w, 1, 3, dop, grid, bins=(5, 17)).values
+    assert t1.is_cuda and np.array_equal(t1.cpu().numpy(), full[5:17])

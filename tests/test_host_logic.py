@@ -70,8 +70,21 @@ def test_filter_and_detection_validation():
                             kst.make_spatial_grid(3, 4))
     with pytest.raises(kst.DimensionError):
         filt.apply_matrix(np.zeros((4, 2), complex))
-    with pytest.raises(NotImplementedError):
-        kst.build_filter("optimal", sigma=np.eye(2), p=1, q=2)
+    # optimal kind: argument / shape errors before any device work
+    # (src/filters.py:144-153; as_matrix's finite check precedes the shape check)
+    with pytest.raises(kst.DimensionError):
+        kst.build_filter("optimal", sigma=np.eye(2), p=1)
+    with pytest.raises(kst.DimensionError):
+        kst.build_filter("optimal", sigma=np.eye(3), p=1, q=2)
+    with pytest.raises(kst.DimensionError):
+        kst.build_filter("optimal", sigma=np.ones(4), p=1, q=2)
+    with pytest.raises(kst.DataError):
+        kst.build_filter("optimal", sigma=np.full((3, 3), np.nan), p=1, q=2)
+    with pytest.raises(kst.DimensionError):
+        kst.make_steering(0.1, 0, 4)
+    sv = kst.make_steering(0.0, 4, 8)
+    assert np.array_equal(sv.spatial, np.ones(4))
+    assert abs(np.linalg.norm(sv.vector) - 1.0) < 1e-12
     with pytest.raises(kst.DimensionError):
         kst.build_filter("bogus")
 

@@ -126,3 +126,19 @@ def test_scenes_are_bit_exact_with_reference_simulator():
         hist = scenes.gen_clutter(cfg) if k == 1 and not gkw else scenes.gen_multipass(cfg, k, **gkw)
         hist = scenes.inject_target(hist, 3, 0.25, 2.0 - 1.0j, pass_index=k - 1)
         assert hashlib.sha256(np.ascontiguousarray(hist.data).tobytes()).hexdigest() == str(want)
+
+
+def test_oracle_optimal_and_sinr():
+    """oracle.optimal_whiten / steering / sinr against the reference's
+    build_filter("optimal"), detection_image, make_steering and sinr outputs
+    (oracle/gen_golden.py optimal_cases)."""
+    g = golden("optimal_cases")
+    sigma, cube = g["sigma"], g["cube"]
+    wh = orc.optimal_whiten(sigma, cube)
+    assert np.abs(wh - g["whitened"]).max() <= 1e-12 * np.abs(g["whitened"]).max()
+    m = orc.detect("kron", None, None, wh, orc.doppler_grid(32), orc.spatial_grid(3, 8))
+    assert np.abs(m - g["map"]).max() <= 1e-12 * np.abs(g["map"]).max()
+    sv = orc.steering(0.25, 3, 32, kappa=2.0)
+    assert np.abs(sv - g["steering"]).max() <= 1e-15
+    w_opt = orc.optimal_whiten(sigma, sv.reshape(1, 3, 32)).ravel()
+    assert abs(orc.sinr(w_opt, sv, 2.0, sigma) - g["sinr"][2]) <= 1e-10 * g["sinr"][2]

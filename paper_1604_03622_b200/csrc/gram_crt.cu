@@ -516,6 +516,44 @@ __host__ __device__ __forceinline__ void upper_tile(int t, int T, int& I, int& J
   J = i + (t - (i * T - i * (i - 1) / 2));
 }
 
+// Visiting order of the persistent kernel: bands of KST_TC_BAND tile rows,
+// each walked column by column (the diagonal triangle first), so the 148
+// tiles in flight cover a ~12 x 12 block of the grid and each operand tile
+// is fetched from HBM about once per band instead of once per tile row
+// (row-major order re-reads every column tile T times once the residues
+// outgrow L2: 92 GB at d = 24012). Results are stored by the row-major
+// index (upper_tile), so only the order changes.
+#ifndef KST_TC_BAND
+#define KST_TC_BAND 12
+#endif
+__host__ __device__ __forceinline__ void band_tile(int v, int T, int& I, int& J) {
+  int b0 = 0;
+  for (;;) {
+    const int h = T - b0 < KST_TC_BAND ? T - b0 : KST_TC_BAND;
+    const int tri = h * (h + 1) / 2;
+    const int cnt = tri + (T - b0 - h) * h;
+    if (v < cnt) {
+      if (v < tri) {  // triangle, column c holds rows b0 .. b0 + c
+        int c = (int)((sqrt(8.0 * v + 1.0) - 1.0) * 0.5);
+        while (c > 0 && c * (c + 1) / 2 > v) --c;
+        while ((c + 1) * (c + 2) / 2 <= v) ++c;
+        J = b0 + c;
+        I = b0 + (v - c * (c + 1) / 2);
+      } else {
+        const int u = v - tri;
+        J = b0 + h + u / h;
+        I = b0 + u % h;
+      }
+      return;
+    }
+    v -= cnt;
+    b0 += h;
+  }
+}
+__host__ __device__ __forceinline__ int upper_index(int I, int J, int T) {
+  return I * T - I * (I - 1) / 2 + (J - I);
+}
+
 // v mod m in [0, m), integer pipes only (no conversions): u = v + m 2^22,
 // q = floor(u / m) = umulhi(u, ceil(2^39 / m)) >> 7, exact for u < 2^31 and
 // 128 < m <= 256 (magic = 2^31 for m = 256). n <= kTcMaxN keeps
@@ -565,9 +603,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int v = blockIdx.x; v < ntiles; v += gridDim.x) {
         int I, J;
-        upper_tile(t, T, I, J);
+        band_tile(v, T, I, J);
         for (int i = 0; i < nmod; ++i)
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             const int s = it % TC_STAGES;
@@ -661,7 +699,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
     const int row = q * 32 + lane;
     const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + 32 * cb;
     int pass = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+    for (int v = blockIdx.x; v < ntiles; v += gridDim.x) {
+      int I, J;
+      band_tile(v, T, I, J);
+      const int t = upper_index(I, J, T);
       for (int i = 0; i < nmod; ++i, ++pass) {
         mbar_wait(tfull, (uint32_t)pass & 1u);
         tc_fence_after();
@@ -696,6 +737,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) gram_tc_kernel(
         dim[0] = make_uint4(pim[0], pim[1], pim[2], pim[3]);
         dim[1] = make_uint4(pim[4], pim[5], pim[6], pim[7]);
       }
+    }
   }
   tc_fence_before();
   __syncthreads();

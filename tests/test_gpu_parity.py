@@ -271,7 +271,8 @@ def test_crt_gram_engine_error_bound(nmod):
     assert np.linalg.norm(s - ref) <= bound * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("shape", [(3, 256, 256), (3, 100, 77), (2, 300, 1000), (1, 40, 3)])
+@pytest.mark.parametrize("shape", [(3, 256, 256), (3, 100, 77), (2, 300, 1000), (1, 40, 3),
+                                   (2, 1700, 300)])
 @pytest.mark.parametrize("nmod", [9, 10, 13])
 def test_crt_tcgen05_kernel_matches_library_gemm_path(shape, nmod):
     """The hand-written tcgen05 CRT Gram (mode "crt") against the same CRT

@@ -55,13 +55,20 @@ __global__ void __launch_bounds__(NT) stats_kernel(const cplx* __restrict__ S, i
     const cplx* row = S + a * d;
 #pragma unroll
     for (int j = 0; j < P; ++j) {
-      for (int c = threadIdx.x; c < q; c += NT) {
-        const cplx v = row[(int64_t)j * q + c];
-        if (!isfinite(v.x) || !isfinite(v.y)) bad += 1.0;
-        fro = fma(v.x, v.x, fro);
-        fro = fma(v.y, v.y, fro);
-        bs[2 * j] += v.x;
-        bs[2 * j + 1] += v.y;
+      // four independent streaming loads in flight per thread (S is read once here)
+      for (int c0 = threadIdx.x; c0 < q; c0 += 4 * NT) {
+        cplx v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = (c0 + u * NT < q) ? __ldcs(&row[(int64_t)j * q + c0 + u * NT]) : cmk(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (!isfinite(v[u].x) || !isfinite(v[u].y)) bad += 1.0;
+          fro = fma(v[u].x, v[u].x, fro);
+          fro = fma(v[u].y, v[u].y, fro);
+          bs[2 * j] += v[u].x;
+          bs[2 * j + 1] += v[u].y;
+        }
       }
     }
     if (threadIdx.x == 0) {

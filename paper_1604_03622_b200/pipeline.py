@@ -59,7 +59,10 @@ class FrameStream:
     download stream once its frame is done, so the two PCIe directions (two
     copy engines) overlap each other and the compute. With pinned host buffers
     the traffic (192 MB in + 32 MB out per Gotcha frame) hides under the
-    compute up to the host-to-device bandwidth.
+    compute up to the host-to-device bandwidth. `nbuf` device cube buffers
+    (default 3) let the upload of frame i+1 start as soon as frame i-2 is
+    done, so the copy engine never waits on a frame whose compute (with its
+    host round trips) ran long; with 2 it waits for frame i-1.
 
         fs = FrameStream(shape, device)
         for i, cube in enumerate(host_cubes):
@@ -68,22 +71,28 @@ class FrameStream:
     """
 
     def __init__(self, shape, device=None, rank_spatial=1, rank_temporal=3, dopplers=None,
-                 spatial_grid=None, tol=1e-4, max_iter=100, kind="kron", out_pinned=None):
+                 spatial_grid=None, tol=1e-4, max_iter=100, kind="kron", out_pinned=None, nbuf=3):
         import torch
         self.dev = torch.device("cuda", nat.device_index(device))
         n, p, q = shape
+        if nbuf < 2:
+            raise ValueError("FrameStream needs at least 2 buffers")
+        self.nbuf = nbuf
         self.args = (rank_spatial, rank_temporal, dopplers, spatial_grid, tol, max_iter, kind)
         D = q if dopplers is None else len(np.asarray(dopplers).ravel())
-        self.bufs = [torch.empty(shape, dtype=torch.complex128, device=self.dev) for _ in range(2)]
-        self.outs = [torch.empty((1, n, D), dtype=torch.float64, device=self.dev) for _ in range(2)]
+        self.bufs = [torch.empty(shape, dtype=torch.complex128, device=self.dev) for _ in range(nbuf)]
+        self.outs = [torch.empty((1, n, D), dtype=torch.float64, device=self.dev)
+                     for _ in range(nbuf)]
         self.host_out = out_pinned if out_pinned is not None else [
-            torch.empty((n, D), dtype=torch.float64).pin_memory() for _ in range(2)]
+            torch.empty((n, D), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+        if len(self.host_out) < nbuf:
+            raise ValueError(f"out_pinned needs {nbuf} host buffers")
         self.copy = torch.cuda.Stream(self.dev)       # host -> device
         self.copy_back = torch.cuda.Stream(self.dev)  # device -> host
         self.comp = torch.cuda.current_stream(self.dev)
-        self.ready = [torch.cuda.Event() for _ in range(2)]
-        self.done = [torch.cuda.Event() for _ in range(2)]
-        self.back = [torch.cuda.Event() for _ in range(2)]
+        self.ready = [torch.cuda.Event() for _ in range(nbuf)]
+        self.done = [torch.cuda.Event() for _ in range(nbuf)]
+        self.back = [torch.cuda.Event() for _ in range(nbuf)]
         self.i = 0
         self.pending = None
         self.summary = np.zeros(8)
@@ -98,7 +107,7 @@ class FrameStream:
     def submit(self, host_cube):
         """Queue one pinned host cube; process the previously queued one."""
         import torch
-        slot = self.i % 2
+        slot = self.i % self.nbuf
         self._upload(host_cube, slot)
         result = self._process_pending()
         self.pending = slot
@@ -111,7 +120,7 @@ class FrameStream:
             return None
         slot = self.pending
         self.comp.wait_event(self.ready[slot])
-        self.comp.wait_event(self.back[slot])  # map buffer read back (frame i - 2)
+        self.comp.wait_event(self.back[slot])  # map buffer read back (frame i - nbuf)
         process_frame_device(self.bufs[slot], *self.args, out=self.outs[slot], summary=self.summary)
         self.done[slot].record(self.comp)
         with torch.cuda.stream(self.copy_back):

@@ -18,13 +18,31 @@ windows) are detected together in one call.
 
 from __future__ import annotations
 
+import threading
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 from . import _native as nat
 from .errors import DimensionError
 from .filters import DetectionMap, _host_grid_args, build_filter, run_detect
 from .layout import cube_to_snapshots
-from .lrkron import lr_kron_estimate, sample_covariance
+from .lrkron import get_gram_engine, lr_kron_estimate, sample_covariance, set_gram_engine
+
+
+_local = threading.local()
+_pools = {}
+_pool_lock = threading.Lock()
+
+
+def _pool(n):
+    """Process-wide worker threads for concurrent windows (kept alive so each
+    thread's kst context, workspace and stream are created once)."""
+    with _pool_lock:
+        p = _pools.get(n)
+        if p is None:
+            p = _pools[n] = ThreadPoolExecutor(max_workers=n, thread_name_prefix="kst-window")
+        return p
 
 
 def window_start(m, n_w, n_bins):
@@ -50,7 +68,7 @@ def halo_range(lo, hi, n_w, n_bins):
 
 def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, spatial_grid,
                              kind="kron", tol=1e-4, max_iter=100, drop_temporal=False,
-                             return_estimates=False, bins=None):
+                             return_estimates=False, bins=None, workers=4):
     """Detection map of the windowed (L-mode) estimator; cube (n_bins, p, q).
 
     Returns a DetectionMap (host arrays for numpy input, device tensor values
@@ -59,7 +77,8 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
     bins [lo, hi) (map rows lo..hi-1, shape (hi - lo, D)); a host cube then
     has only the tile plus its halo (`halo_range`) copied to the device, so
     a tile-sharded frame moves each bin to at most the GPUs whose windows
-    read it.
+    read it. `workers` host threads estimate windows concurrently (results
+    are identical for any value).
     """
     import torch
     shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
@@ -75,18 +94,59 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
     dev_out = nat.is_device(cube)
     D = int(np.asarray(dopplers.cpu() if nat.is_device(dopplers) else dopplers).size)
     vals = torch.empty((hi - lo, D), dtype=torch.float64, device=x.device)
-    ests = []
-    dop = grid = None
-    for s in range(window_start(lo, n_w, n_bins), window_start(hi - 1, n_w, n_bins) + 1):
+    starts = list(range(window_start(lo, n_w, n_bins), window_start(hi - 1, n_w, n_bins) + 1))
+    ests = {}
+    grids = {}
+
+    def one_window(s):
         scm = sample_covariance(snaps[s - a:s - a + n_w], p, q)
         est = lr_kron_estimate(scm, rank_spatial, rank_temporal, tol=tol, max_iter=max_iter)
         filt = build_filter(kind, estimate=est, drop_temporal=drop_temporal)
-        if dop is None:
-            dop, grid = _host_grid_args(filt, dopplers, spatial_grid)
+        if "dop" not in grids:
+            grids["dop"], grids["grid"] = _host_grid_args(filt, dopplers, spatial_grid)
         t0, t1 = window_bins(s, n_w, n_bins)
         t0, t1 = max(t0, lo), min(t1, hi)
-        vals[t0 - lo:t1 - lo] = run_detect(filt, x[t0 - a:t1 - a], dop, grid)[0]
+        vals[t0 - lo:t1 - lo] = run_detect(filt, x[t0 - a:t1 - a], grids["dop"], grids["grid"])[0]
         if return_estimates:
-            ests.append((s, est))
+            ests[s] = est
+
+    # the first window runs alone (it uploads the device-global constant
+    # plans); the rest run on `workers` host threads, each with its own CUDA
+    # stream and kst context (one ctx per device and thread, include/kst_b200.h),
+    # so the small per-window kernels and host round trips of different
+    # windows overlap. Every window is computed exactly as in the serial loop.
+    one_window(starts[0])
+    rest = starts[1:]
+    nw = max(1, min(int(workers), len(rest)))
+    if nw == 1:
+        for s in rest:
+            one_window(s)
+    else:
+        main = torch.cuda.current_stream(x.device)
+        engine = get_gram_engine(x.device)  # the caller's K1 engine, for every worker
+        pool = _pool(nw)
+        local = _local
+
+        def worker(k):
+            # persistent pool threads: their kst contexts and streams are reused
+            torch.cuda.set_device(x.device)
+            if get_gram_engine(x.device) != engine:
+                set_gram_engine(*engine, device=x.device)
+            streams = local.__dict__.setdefault("streams", {})
+            st = streams.get(x.device.index)
+            if st is None:
+                st = streams[x.device.index] = torch.cuda.Stream(x.device)
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                for s in rest[k::nw]:
+                    one_window(s)
+            return st
+
+        futs = [pool.submit(worker, k) for k in range(nw)]
+        done = [f.result() for f in futs]  # re-raises a worker's exception here
+        for st in done:
+            main.wait_stream(st)
+    dop, grid = grids["dop"], grids["grid"]
+    ests = [(s, ests[s]) for s in starts] if return_estimates else []
     dmap = DetectionMap(vals if dev_out else nat.to_host(vals), dop, grid)
     return (dmap, ests) if return_estimates else dmap

@@ -85,3 +85,24 @@ def test_bin_tiles_with_halo_equal_the_full_frame(world, n_w):
     dev = torch.from_numpy(cube).cuda()
     t1 = kst.windowed_detection_image(dev, n_w, 1, 3, dop, grid, bins=(5, 17)).values
     assert t1.is_cuda and np.array_equal(t1.cpu().numpy(), full[5:17])
+
+
+@pytest.mark.parametrize("workers", [1, 3, 8])
+def test_concurrent_windows_are_bitwise_serial(workers):
+    """Windows estimated on concurrent host threads / streams give exactly the
+    serial loop's map and estimates."""
+    p, q, nb, D, G, n_w = 3, 64, 48, 64, 16, 9
+    cube = scenes.bench_scene(p, q, nb, seed=31, movers=4).data[0]
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    ref, ref_est = kst.windowed_detection_image(cube, n_w, 1, 3, dop, grid, workers=1,
+                                                return_estimates=True)
+    for _ in range(2):
+        got, est = kst.windowed_detection_image(cube, n_w, 1, 3, dop, grid, workers=workers,
+                                                return_estimates=True)
+        assert np.array_equal(got.values, ref.values)
+        assert [s for s, _ in est] == [s for s, _ in ref_est]
+        for (_, e1), (_, e2) in zip(est, ref_est):
+            assert e1.iterations == e2.iterations and e1.residuals == e2.residuals
+            h = [e.spatial.cpu().numpy() if torch.is_tensor(e.spatial) else e.spatial
+                 for e in (e1, e2)]
+            assert np.array_equal(h[0], h[1])

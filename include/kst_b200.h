@@ -186,6 +186,24 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
                  int G, int groups, double* values, double* summary,
                  void* stream);
 
+/*
+ * Windowed (L-mode) estimator, one call for a run of windows (SURVEY.md §8
+ * "L-mode definition"; the reference has no windowed mode -- each window is
+ * its README sequence, pkg/README.md:144-161: sample_covariance
+ * (src/lrkron.py:53) -> lr_kron_estimate (src/lrkron.py:118) -> build_filter
+ * (src/filters.py:137) -> detection_image (src/filters.py:243)).
+ *   cube dev: frame bins [a, a + rows) (n_bins in the frame), (rows, p, q);
+ *   windows s = s_begin, s_begin + s_step, ... < s_end train on bins
+ *   [s, s + n_w) and detect the test bins whose window is s, clipped to the
+ *   tile [lo, hi); values dev (hi - lo, D) float64 (row 0 = bin lo).
+ */
+int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins,
+                 int p, int q, int n_w, int64_t lo, int64_t hi, int64_t s_begin,
+                 int64_t s_end, int64_t s_step, int rank_spatial,
+                 int rank_temporal, double tol, int max_iter, int kind,
+                 int drop_temporal, const double* dopplers, int D,
+                 const double* grid, int G, double* values, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -302,4 +302,51 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   return KST_OK;
 }
 
+int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins, int p, int q, int n_w,
+                 int64_t lo, int64_t hi, int64_t s_begin, int64_t s_end, int64_t s_step,
+                 int rank_spatial, int rank_temporal, double tol, int max_iter, int kind,
+                 int drop_temporal, const double* dopplers, int D, const double* grid, int G,
+                 double* values, void* stream) {
+  CTX_GUARD(ctx);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t d = (int64_t)p * q;
+  if (p < 1 || q < 1 || n_w < 1 || n_w > n_bins || lo < 0 || hi > n_bins || lo >= hi || s_step < 1 ||
+      a < 0 || a > lo)
+    return set_err(ctx, KST_ERR_DIMENSION, "windowed: bad window / tile arguments");
+  if (rank_temporal == q)  // the fused path keeps only the top rb eigenvectors of b
+    return set_err(ctx, KST_ERR_DIMENSION, "windowed: rank_temporal == q needs the step API");
+  cplx* S = (cplx*)ws_get(ctx, WS_S, sizeof(cplx) * d * d);
+  cplx* spatial = (cplx*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 2 + 64);
+  cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal + 64);
+  if (!S || !spatial || !ub) return set_err(ctx, KST_ERR_CUDA, "windowed: workspace");
+  cplx* ua = spatial + p * p;
+  std::vector<double> tbv(rank_temporal > 0 ? rank_temporal : 1);
+  const cplx* X = (const cplx*)cube;  // bin a of the frame at row 0
+  const int h = n_w / 2;
+  for (int64_t s = s_begin; s < s_end; s += s_step) {
+    if (s < 0 || s + n_w > n_bins || s < a)
+      return set_err(ctx, KST_ERR_DIMENSION, "windowed: window %lld outside the cube",
+                     (long long)s);
+    // training: bins [s, s + n_w) (SURVEY.md §8 L-mode definition)
+    KST_TRY(kst::scm(ctx, X + (s - a) * d, n_w, d, S, st));
+    kst::FitOut fit;
+    std::fill(tbv.begin(), tbv.end(), 0.0);
+    KST_TRY(kst::lrkron(ctx, S, p, q, rank_spatial, rank_temporal, tol, max_iter, 1, spatial,
+                        nullptr, ub, tbv.data(), &fit, nullptr, nullptr, st));
+    int ka = 0, kb = 0;
+    KST_TRY(kst::subspace_basis(ctx, spatial, p, rank_spatial, 1e-9, ua, &ka, st));
+    if (tbv[0] > 0.0)
+      while (kb < rank_temporal && tbv[kb] > 1e-9 * tbv[0]) ++kb;
+    // test bins sharing window s (windowed.window_bins), clipped to the tile
+    int64_t t0 = (s == 0) ? 0 : s + h, t1 = (s == n_bins - n_w) ? n_bins : s + h + 1;
+    t0 = std::max(t0, lo);
+    t1 = std::min(t1, hi);
+    if (t1 <= t0) continue;
+    KST_TRY(kst::detect(ctx, X + (t0 - a) * d, t1 - t0, p, q, ka ? ua : nullptr, ka,
+                        kb ? ub : nullptr, kb, kind, drop_temporal, dopplers, D,
+                        (const cplx*)grid, G, 1, values + (t0 - lo) * D, st, false));
+  }
+  return KST_OK;
+}
+
 }  // extern "C"

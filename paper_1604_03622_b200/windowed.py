@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as nat
 from .errors import DimensionError
-from .filters import DetectionMap, _host_grid_args, build_filter, run_detect
+from .filters import DetectionMap, StapFilter, _host_grid_args, build_filter, run_detect
 from .layout import cube_to_snapshots
 from .lrkron import get_gram_engine, lr_kron_estimate, sample_covariance, set_gram_engine
 
@@ -68,7 +68,7 @@ def halo_range(lo, hi, n_w, n_bins):
 
 def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, spatial_grid,
                              kind="kron", tol=1e-4, max_iter=100, drop_temporal=False,
-                             return_estimates=False, bins=None, workers=4):
+                             return_estimates=False, bins=None, workers=8):
     """Detection map of the windowed (L-mode) estimator; cube (n_bins, p, q).
 
     Returns a DetectionMap (host arrays for numpy input, device tensor values
@@ -97,8 +97,28 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
     starts = list(range(window_start(lo, n_w, n_bins), window_start(hi - 1, n_w, n_bins) + 1))
     ests = {}
     grids = {}
+    # estimates not requested: every window runs inside one C call per worker
+    # (kst_windowed: scm -> lrkron -> bases -> detect per window, no Python
+    # per window); the step-API loop below keeps the per-window estimates
+    fused = not return_estimates and rank_temporal < q and kind in nat.KIND
+    if fused:
+        grids["dop"], grids["grid"] = _host_grid_args(StapFilter(kind, p, q), dopplers, spatial_grid)
+        xc = x.contiguous()
+
+    def run_fused(s_begin, s_end, step):
+        dop, grid = grids["dop"], grids["grid"]
+        c = nat.ctx(x.device)
+        nat.check(nat.lib().kst_windowed(
+            c, nat.ptr(xc), a, n_bins, p, q, n_w, lo, hi, s_begin, s_end, step,
+            int(rank_spatial), int(rank_temporal), float(tol), int(max_iter), nat.KIND[kind],
+            int(bool(drop_temporal)), dop.ctypes.data_as(nat.C.c_void_p), dop.size,
+            grid.ctypes.data_as(nat.C.c_void_p), grid.shape[0], nat.ptr(vals),
+            nat.stream_of(x.device)), c)
 
     def one_window(s):
+        if fused:
+            run_fused(s, s + 1, 1)
+            return
         scm = sample_covariance(snaps[s - a:s - a + n_w], p, q)
         est = lr_kron_estimate(scm, rank_spatial, rank_temporal, tol=tol, max_iter=max_iter)
         filt = build_filter(kind, estimate=est, drop_temporal=drop_temporal)
@@ -138,8 +158,11 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
                 st = streams[x.device.index] = torch.cuda.Stream(x.device)
             st.wait_stream(main)
             with torch.cuda.stream(st):
-                for s in rest[k::nw]:
-                    one_window(s)
+                if fused:
+                    run_fused(rest[k], rest[-1] + 1, nw)
+                else:
+                    for s in rest[k::nw]:
+                        one_window(s)
             return st
 
         futs = [pool.submit(worker, k) for k in range(nw)]

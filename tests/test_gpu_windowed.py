@@ -106,3 +106,25 @@ def test_concurrent_windows_are_bitwise_serial(workers):
             h = [e.spatial.cpu().numpy() if torch.is_tensor(e.spatial) else e.spatial
                  for e in (e1, e2)]
             assert np.array_equal(h[0], h[1])
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+@pytest.mark.parametrize("kind,drop", [("kron", False), ("classical", False), ("kron", True)])
+def test_fused_windows_equal_the_step_api_loop(workers, kind, drop):
+    """kst_windowed (one C call per worker, no per-window Python) gives the
+    step-API loop's map bitwise, also for a tile with halo."""
+    p, q, nb, D, G, n_w = 3, 64, 40, 48, 8, 9
+    cube = scenes.bench_scene(p, q, nb, seed=41, movers=3).data[0]
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    kw = dict(kind=kind, drop_temporal=drop)
+    ref = kst.windowed_detection_image(cube, n_w, 1, 3, dop, grid, return_estimates=True, workers=1,
+                                       **kw)[0].values
+    got = kst.windowed_detection_image(cube, n_w, 1, 3, dop, grid, workers=workers, **kw).values
+    assert np.array_equal(got, ref)
+    tile = kst.windowed_detection_image(cube, n_w, 1, 3, dop, grid, bins=(7, 30), workers=workers,
+                                        **kw).values
+    assert np.array_equal(tile, ref[7:30])
+    bad = cube.copy()
+    bad[12, 1, 5] = np.nan
+    with pytest.raises(kst.DataError):
+        kst.windowed_detection_image(bad, n_w, 1, 3, dop, grid, workers=workers, **kw)

@@ -19,7 +19,11 @@
  *    layer maps onto the reference's exception classes (src/errors.py:9-30).
  *    No C++ exception crosses this boundary. kst_last_error() gives text.
  *  - One kst_ctx per (device, host thread). The context owns a grow-only
- *    device workspace; callers own every input/output buffer.
+ *    device workspace; callers own every input/output buffer. Contexts on
+ *    different threads/streams may run concurrently; the small FFT / CRT
+ *    plans live in device-global constant memory and are uploaded once per
+ *    distinct plan, so concurrent callers should share shapes (the windowed
+ *    estimator runs its first window alone, then fans out).
  *  - Results are deterministic: fixed-order reductions, no float atomics.
  */
 #ifndef KST_B200_H

@@ -1015,7 +1015,9 @@ __global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
 }
 
 // host: is grid[g, i] = exp(2 pi i (g / G) i) / sqrt(p) (make_spatial_grid,
-// src/filters.py:208-217) to within rounding
+// src/filters.py:208-217) to within rounding (numpy rounds the phase
+// 2 pi (g / G) i before exp: ~1e-15 absolute; 1e-12 separates the uniform
+// grid from any other while staying far inside the map tolerance)
 bool dft_grid(const cplx* grid, int G, int p) {
   const long double pi = 3.141592653589793238462643383279502884L;
   const long double s = 1.0L / sqrtl((long double)p);
@@ -1024,7 +1026,7 @@ bool dft_grid(const cplx* grid, int G, int p) {
       const long double th = 2.0L * pi * ((long double)g / G) * i;
       const long double dx = (long double)grid[g * p + i].x - s * cosl(th);
       const long double dy = (long double)grid[g * p + i].y - s * sinl(th);
-      if (fabsl(dx) > 4e-16L || fabsl(dy) > 4e-16L) return false;
+      if (fabsl(dx) > 1e-12L || fabsl(dy) > 1e-12L) return false;
     }
   return true;
 }

@@ -116,7 +116,13 @@ __global__ void __launch_bounds__(128) bz_kernel(const cplx* __restrict__ B, int
 // thread i streams column i of B down rows k (coalesced across the warp, each
 // element read once, 8 loads in flight per thread), Z rows broadcast from
 // shared memory. Split-K over blockIdx.y; partials summed in fixed order.
-constexpr int BZ2_COLS = 128;
+#ifndef KST_BZ2_U
+#define KST_BZ2_U 8  // rows of B in flight per thread
+#endif
+#ifndef KST_BZ2_COLS
+#define KST_BZ2_COLS 128
+#endif
+constexpr int BZ2_COLS = KST_BZ2_COLS;
 #ifndef KST_BZ2_K8
 #define KST_BZ2_K8 128
 #endif
@@ -143,12 +149,12 @@ __global__ void __launch_bounds__(BZ2_COLS) bz2_kernel(const cplx* __restrict__ 
   if (i < n) {
     const cplx* col = B + i;
     int k = kbeg;
-    for (; k + 8 <= kend; k += 8) {
-      cplx bv[8];
+    for (; k + KST_BZ2_U <= kend; k += KST_BZ2_U) {
+      cplx bv[KST_BZ2_U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) bv[u] = col[(size_t)(k + u) * n];
+      for (int u = 0; u < KST_BZ2_U; ++u) bv[u] = col[(size_t)(k + u) * n];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < KST_BZ2_U; ++u) {
         const cplx* zr = sz + (k + u - kbeg) * S;
 #pragma unroll
         for (int c = 0; c < S; ++c) cfma(acc[c], zr[c], bv[u]);
@@ -355,8 +361,22 @@ __global__ void __launch_bounds__(1024) finalize_top_kernel(
     const int k = threadIdx.x % s, g = threadIdx.x / s;
     double bm = -1.0;
     int bi = n;
-    if (g < ng)
-      for (int i = g; i < n; i += ng) {
+    if (g < ng) {
+      int i = g;
+      for (; i + 3 * ng < n; i += 4 * ng) {  // four loads in flight, rows in ascending order
+        cplx v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = Z[(size_t)(i + u * ng) * s + k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double a = hypot(v[u].x, v[u].y);
+          if (a > bm) {
+            bm = a;
+            bi = i + u * ng;
+          }
+        }
+      }
+      for (; i < n; i += ng) {
         const cplx v = Z[(size_t)i * s + k];
         const double a = hypot(v.x, v.y);
         if (a > bm) {
@@ -364,6 +384,7 @@ __global__ void __launch_bounds__(1024) finalize_top_kernel(
           bi = i;
         }
       }
+    }
     sbm[threadIdx.x] = bm;
     sbi[threadIdx.x] = bi;
     __syncthreads();

@@ -669,6 +669,10 @@ constexpr int FB_NT = KST_FB_NT;
 constexpr int FB_MAXP = 4;
 constexpr int FB_MAXKB = 4;
 constexpr int FB_MAXG = 64;
+#ifndef KST_FB_PDT
+#define KST_FB_PDT 2
+#endif
+constexpr int FB_PDT = KST_FB_PDT;  // Parseval: d values per thread with loads in flight
 
 struct FusedArgs {
   int P, q, D, ka, kb, G, groups, mode, spatial;
@@ -895,17 +899,32 @@ __global__ void __launch_bounds__(FB_NT, 1) detect_bin_kernel(
       double acc[2 * NC];
 #pragma unroll
       for (int c = 0; c < 2 * NC; ++c) acc[c] = 0.0;
-      for (int d = tid; d < D; d += FB_NT) {
+      // the basis spectra come from L2 (__ldcg: L1 keeps the twiddles): all
+      // FB_PDT x kb loads of a chunk are issued before its FMAs, so the L2
+      // latency is paid once per chunk, not once per d (same summation order)
+      for (int d0 = tid; d0 < D; d0 += FB_PDT * FB_NT) {
+        cplx u[FB_PDT][FB_MAXKB];
 #pragma unroll
-        for (int k = 0; k < FB_MAXKB; ++k) {
-          if (k < fa.kb) {
-            const cplx u = __ldcg(&ubspec[(int64_t)k * D + d]);  // L2 only: L1 keeps the twiddles
+        for (int t = 0; t < FB_PDT; ++t)
 #pragma unroll
-            for (int i = 0; i < P; ++i) {
-              cplx c = cmk(acc[2 * (i * FB_MAXKB + k)], acc[2 * (i * FB_MAXKB + k) + 1]);
-              cfmac(c, X[(size_t)i * D + d], u);
-              acc[2 * (i * FB_MAXKB + k)] = c.x;
-              acc[2 * (i * FB_MAXKB + k) + 1] = c.y;
+          for (int k = 0; k < FB_MAXKB; ++k) {
+            const int d = d0 + t * FB_NT;
+            u[t][k] = (k < fa.kb && d < D) ? __ldcg(&ubspec[(int64_t)k * D + d]) : cmk(0.0, 0.0);
+          }
+#pragma unroll
+        for (int t = 0; t < FB_PDT; ++t) {
+          const int d = d0 + t * FB_NT;
+          if (d >= D) break;
+#pragma unroll
+          for (int k = 0; k < FB_MAXKB; ++k) {
+            if (k < fa.kb) {
+#pragma unroll
+              for (int i = 0; i < P; ++i) {
+                cplx c = cmk(acc[2 * (i * FB_MAXKB + k)], acc[2 * (i * FB_MAXKB + k) + 1]);
+                cfmac(c, X[(size_t)i * D + d], u[t][k]);
+                acc[2 * (i * FB_MAXKB + k)] = c.x;
+                acc[2 * (i * FB_MAXKB + k) + 1] = c.y;
+              }
             }
           }
         }

@@ -162,7 +162,8 @@ int kst_filter(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
  * kst_chol replaces build_filter(kind="optimal") (src/filters.py:144-163:
  *   as_matrix finite check, then scipy cho_factor(sigma, lower=True)):
  *   sigma dev (d, d) complex row-major, only its lower triangle is read;
- *   L dev (d, d) complex receives the column-major lower Cholesky factor.
+ *   L dev (d, d) complex (not aliasing sigma) receives the column-major
+ *   lower Cholesky factor.
  *   KST_ERR_DATA if sigma has a non-finite entry or is not positive definite.
  * kst_chol_solve replaces StapFilter.apply_matrix for kind "optimal"
  *   (src/filters.py:98-100: cho_solve): X = sigma^-1 B for every column of the

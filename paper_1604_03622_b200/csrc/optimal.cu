@@ -104,6 +104,8 @@ extern "C" int kst_chol(kst_ctx* ctx, const double* sigma, int d, double* L, voi
   if (!ctx) return KST_ERR_DIMENSION;
   ctx->err.clear();
   if (d < 1) return set_err(ctx, KST_ERR_DIMENSION, "chol: dimension %d", d);
+  if ((const void*)sigma == (const void*)L)  // the tiled transpose cannot run in place
+    return set_err(ctx, KST_ERR_DIMENSION, "chol: L must not alias sigma");
   cudaStream_t st = (cudaStream_t)stream;
   cplx* A = (cplx*)L;
   int* dflag = (int*)ws_get(ctx, WS_SMALL, 64);

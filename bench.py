@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="gotcha", choices=sorted(CONFIGS) + ["lmode", "multipass"])
+    ap.add_argument("--config", default="gotcha",
+                    choices=sorted(CONFIGS) + ["lmode", "multipass", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -332,6 +333,76 @@ def run_lmode(args, rank, local, world):
                          "the eigen stages); the frame headline is configs[1]"}))
 
 
+def run_sweep(args, rank, local, world):
+    """Supplementary line for configs[3]'s sweep (SURVEY.md §8 cfg 4): L-mode
+    window n_w in {9, 25, 49, 81} (3x3 .. 9x9 training snapshots) x ranks
+    (r_a, r_b) in {1, 2, 3}^2 on the 256 x 256 frame, plus the global
+    estimate at each rank pair; 256-bin Doppler bank x 16 spatial steering
+    candidates. One frame per point per step; value = all pixels of the
+    sweep / its device time. r_a = p = 3 makes the map identically zero
+    (SURVEY.md §8 window parity note): those points are timed and flagged.
+    N > 1 runs the sweep on every rank (replicas)."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1604_03622_b200 as kst
+    p, q, nb, D, G = 3, 256, 256, 256, 16
+    host = make_frame((p, q, nb, D, G, 1, 3, 1), 17 + rank)
+    cube = torch.from_numpy(host).to(dev)
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    points = [(n_w, ra, rb) for n_w in (9, 25, 49, 81, None) for ra in (1, 2, 3) for rb in (1, 2, 3)]
+
+    def run(pt):
+        n_w, ra, rb = pt
+        if n_w is None:
+            vals, _ = kst.process_frame_device(cube, ra, rb, dop, grid)
+            return vals
+        return kst.windowed_detection_image(cube, n_w, ra, rb, dop, grid).values
+
+    for pt in points[: max(1, args.warmup)]:
+        run(pt)
+    rows, tot_ms = [], 0.0
+    for pt in points:
+        run(pt)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            v = run(pt)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / args.steps
+        tot_ms += ms
+        rows.append({"n_w": pt[0] or "global", "r_a": pt[1], "r_b": pt[2], "ms": ms,
+                     "pixels_per_s": nb * D / (ms / 1e3),
+                     "map_max": float(v.max()), "zero_map": pt[1] == p})
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t[0])
+    if rank == 0:
+        px = nb * D * len(points) * world
+        print(json.dumps({
+            "metric": "STAP pixels/sec", "value": px / (tot_ms / 1e3), "unit": "pixels/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128/f64",
+            "data": "synthetic (reference simulator restated in scenes.py; seeded, 8 movers)",
+            "config": {"workload": "configs[3] sweep: L-mode n_w in {9,25,49,81} + global, ranks "
+                                   "(r_a, r_b) in {1,2,3}^2, 256 x 256 frame, 256 Doppler x 16 "
+                                   "spatial; a step = the whole 45-point sweep",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "sweep": rows, "roofline": None,
+            "roofline_note": "latency-bound per-window kernels; the frame headline is configs[1]"}),
+            flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_multipass(args, rank, local, world):
     """Supplementary line for configs[4] (SURVEY.md §8 cfg 5): a 4-pass
     3-channel 2001 x 2001 stack per GPU per step, stacked to (n, 12, q),
@@ -424,6 +495,9 @@ def run_multipass(args, rank, local, world):
 
 def main():
     args = parse()
+    if args.config == "sweep" and args.impl == "ours":
+        run_sweep(args, *dist_env())
+        return
     if args.config == "lmode" and args.impl == "ours":
         run_lmode(args, *dist_env())
         return

@@ -441,14 +441,19 @@ def run_multipass(args, rank, local, world):
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     launches = nat.lib().kst_launch_count(c) - l0
-    # end to end: pinned host stack -> HBM, pipeline, maps -> pinned host, every step
-    hmaps = torch.empty((K, n, D), dtype=torch.float64, pin_memory=True)
+    # end to end: pinned host stack -> HBM, pipeline, K maps -> pinned host,
+    # every step; FrameStream overlaps stack i+1's upload and stack i-1's
+    # maps download with stack i's compute
+    from paper_1604_03622_b200.pipeline import FrameStream
+    fs = FrameStream(tuple(host.shape), dev, K, rb, dop, grid, groups=K)
+    fs.submit(host_pin)
+    fs.flush()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cube.copy_(host_pin, non_blocking=True)
-        process_frame_device(cube, K, rb, dop, grid, groups=K, out=out)
-        hmaps.copy_(out, non_blocking=True)
+        fs.submit(host_pin)
+    _, ev = fs.flush()
+    ev.synchronize()
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t0
     if world > 1:

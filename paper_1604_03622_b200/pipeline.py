@@ -71,20 +71,24 @@ class FrameStream:
     """
 
     def __init__(self, shape, device=None, rank_spatial=1, rank_temporal=3, dopplers=None,
-                 spatial_grid=None, tol=1e-4, max_iter=100, kind="kron", out_pinned=None, nbuf=3):
+                 spatial_grid=None, tol=1e-4, max_iter=100, kind="kron", out_pinned=None, nbuf=3,
+                 groups=1):
         import torch
         self.dev = torch.device("cuda", nat.device_index(device))
         n, p, q = shape
         if nbuf < 2:
             raise ValueError("FrameStream needs at least 2 buffers")
         self.nbuf = nbuf
-        self.args = (rank_spatial, rank_temporal, dopplers, spatial_grid, tol, max_iter, kind)
+        self.args = (rank_spatial, rank_temporal, dopplers, spatial_grid, tol, max_iter, kind,
+                     groups)
+        self.groups = groups
         D = q if dopplers is None else len(np.asarray(dopplers).ravel())
         self.bufs = [torch.empty(shape, dtype=torch.complex128, device=self.dev) for _ in range(nbuf)]
-        self.outs = [torch.empty((1, n, D), dtype=torch.float64, device=self.dev)
+        self.outs = [torch.empty((groups, n, D), dtype=torch.float64, device=self.dev)
                      for _ in range(nbuf)]
+        hshape = (n, D) if groups == 1 else (groups, n, D)
         self.host_out = out_pinned if out_pinned is not None else [
-            torch.empty((n, D), dtype=torch.float64).pin_memory() for _ in range(nbuf)]
+            torch.empty(hshape, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
         if len(self.host_out) < nbuf:
             raise ValueError(f"out_pinned needs {nbuf} host buffers")
         self.copy = torch.cuda.Stream(self.dev)       # host -> device
@@ -125,7 +129,8 @@ class FrameStream:
         self.done[slot].record(self.comp)
         with torch.cuda.stream(self.copy_back):
             self.copy_back.wait_event(self.done[slot])
-            self.host_out[slot].copy_(self.outs[slot][0], non_blocking=True)
+            src = self.outs[slot][0] if self.groups == 1 else self.outs[slot]
+            self.host_out[slot].copy_(src, non_blocking=True)
             self.back[slot].record(self.copy_back)
         self.pending = None
         return self.host_out[slot], self.back[slot]

@@ -373,3 +373,27 @@ def test_uniform_spatial_grid_fast_path(p, G):
         got = kst.detection_image(filt, cube, dop, gr).values
         want = orc.detect("kron", ua, ub, cube, dop, gr)
         assert np.abs(got - want).max() <= 1e-11 * m0
+
+
+def test_frame_stream_multipass_groups():
+    """FrameStream with groups = K (pass-stacked cubes, K maps per stack)
+    returns exactly the single-stack pipeline's maps."""
+    from paper_1604_03622_b200 import scenes
+    from paper_1604_03622_b200.pipeline import FrameStream, process_frame_device
+    K, p, q, n = 3, 2, 24, 40
+    stacks = [np.ascontiguousarray(kst.stack_passes(
+        scenes.bench_scene(p, q, n, seed=300 + i, movers=2, n_passes=K)).data) for i in range(3)]
+    dop, grid = kst.make_doppler_grid(q), kst.make_stacked_spatial_grid(p, K, 8)
+    fs = FrameStream(stacks[0].shape, 0, K, 2, dop, grid, groups=K)
+    got = []
+    for s_ in stacks:
+        r = fs.submit(torch.from_numpy(s_).pin_memory())
+        if r is not None:
+            r[1].synchronize()
+            got.append(r[0].numpy().copy())
+    r = fs.flush()
+    r[1].synchronize()
+    got.append(r[0].numpy().copy())
+    for s_, g in zip(stacks, got):
+        want, _ = process_frame_device(torch.from_numpy(s_).cuda(), K, 2, dop, grid, groups=K)
+        assert g.shape == (K, n, q) and np.array_equal(g, want.cpu().numpy())

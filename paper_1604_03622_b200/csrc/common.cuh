@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3: ranges cost ~nothing without a tool
+
 #include "../../include/kst_b200.h"
 
 typedef double2 cplx;  // (re, im) == numpy complex128 memory
@@ -80,12 +82,25 @@ struct kst_ctx {
   std::vector<double> det_key;
   long long launches = 0;
   int profiling = 0;
+  // NVTX ranges of the kst_pipeline stages (kst.scm, kst.lrkron, kst.bases,
+  // kst.detect) and of the Gram's tensor-core span, for ncu --nvtx filters
+  nvtxRangeId_t nvtx_stage = 0, nvtx_sub = 0;
   cudaEvent_t ev[8] = {};
   int n_ev = 0;
 };
 
 // record stage boundary k on `st` when profiling (kst_pipeline)
 inline void stage_mark(kst_ctx* ctx, int k, cudaStream_t st) {
+  static const char* const kStage[4] = {"kst.scm", "kst.lrkron", "kst.bases", "kst.detect"};
+  if (k <= 4) {
+    if (ctx->nvtx_stage) nvtxRangeEnd(ctx->nvtx_stage);
+    ctx->nvtx_stage = k < 4 ? nvtxRangeStartA(kStage[k]) : 0;
+  } else if (k == 5) {
+    ctx->nvtx_sub = nvtxRangeStartA("kst.gram.tensor");
+  } else if (k == 6 && ctx->nvtx_sub) {
+    nvtxRangeEnd(ctx->nvtx_sub);
+    ctx->nvtx_sub = 0;
+  }
   if (!ctx->profiling || k >= 8) return;
   if (!ctx->ev[k]) cudaEventCreate(&ctx->ev[k]);
   cudaEventRecord(ctx->ev[k], st);

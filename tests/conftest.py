@@ -51,3 +51,18 @@ PIPELINE_CASES = ["readme_q16"] + [f"sweep_q64_ra{a}_rb{b}" for a in (1, 2, 3) f
 def map_tolerance(ref, m0, rel=1e-4, floor=1e-5):
     """SURVEY.md §8c map rule: |v - v_ref| <= rel*|v_ref| + floor*M0."""
     return rel * np.abs(ref) + floor * m0
+
+
+def binary_map_mismatch(vals, ref, m0, taus):
+    """north_star / SURVEY.md §8c detection-map rule: the thresholded maps
+    (v >= tau) must be identical except at pixels whose reference statistic
+    lies within the map tolerance of tau. Returns (disallowed mismatches,
+    allowed near-threshold mismatches) summed over the thresholds."""
+    tol = map_tolerance(ref, m0)
+    bad = near = 0
+    for tau in taus:
+        diff = (vals >= tau) != (ref >= tau)
+        band = np.abs(ref - tau) <= tol
+        bad += int(np.count_nonzero(diff & ~band))
+        near += int(np.count_nonzero(diff & band))
+    return bad, near

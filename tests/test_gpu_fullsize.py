@@ -78,3 +78,8 @@ def test_gotcha_frame_matches_oracle(frame, engine):
     assert sp_err <= (1e-9 if (mode, slices) != ("int8", 5) else 1e-8)
     assert pa < 1e-8 and pb < 1e-8
     assert np.all(err <= budget) and np.all(ferr <= budget)
+    # thresholded detection maps: identical except within the tolerance of tau
+    from conftest import binary_map_mismatch
+    taus = list(np.quantile(ref, [0.5, 0.9, 0.99, 0.9999])) + [0.5 * m0]
+    for v in (img.values, fused):
+        assert binary_map_mismatch(v, ref, m0, taus)[0] == 0

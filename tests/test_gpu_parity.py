@@ -397,3 +397,26 @@ def test_frame_stream_multipass_groups():
     for s_, g in zip(stacks, got):
         want, _ = process_frame_device(torch.from_numpy(s_).cuda(), K, 2, dop, grid, groups=K)
         assert g.shape == (K, n, q) and np.array_equal(g, want.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", PIPELINE_CASES)
+def test_detection_maps_identical_off_threshold(name):
+    """Thresholded detection maps (v >= tau, tau at the 50/90/99/99.9 %
+    quantiles of the reference map and at 0.5 M0) equal the reference's
+    except at pixels within the §8c tolerance of tau."""
+    from conftest import binary_map_mismatch
+    d = golden(name)
+    cube = scene_cube(d)
+    n, p, q = cube.shape
+    D, G = int(d["D"]), int(d["G"])
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    scm = kst.sample_covariance(kst.cube_to_snapshots(cube), p, q)
+    est = kst.lr_kron_estimate(scm, int(d["ra"]), int(d["rb"]), tol=float(d["tol"]),
+                               max_iter=int(d["max_iter"]))
+    filt = kst.build_filter(str(d["kind"]), estimate=est, drop_temporal=bool(d["drop_temporal"]))
+    vals = kst.detection_image(filt, cube, dop, grid).values
+    ref = d["values"]
+    m0 = float(d["m0"])
+    taus = list(np.quantile(ref, [0.5, 0.9, 0.99, 0.999])) + [0.5 * m0]
+    bad, near = binary_map_mismatch(vals, ref, m0, taus)
+    assert bad == 0, (bad, near)

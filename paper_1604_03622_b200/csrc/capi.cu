@@ -76,26 +76,6 @@ void* pinned_get(kst_ctx* ctx, size_t bytes) {
   return ctx->pinned;
 }
 
-namespace {
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
-}  // namespace
-
-#define CTX_GUARD(ctx)                          \
-  if (!(ctx)) return KST_ERR_DIMENSION;         \
-  DeviceGuard guard__((ctx)->device);           \
-  (ctx)->err.clear();
-
 extern "C" {
 
 int kst_version(void) { return 1; }

@@ -130,6 +130,27 @@ enum WsSlot {
   WS_OZ_PROD = 19   // int8 Gram: int32 diagonal products
 };
 
+// Every extern "C" entry point runs on its context's device: the caller's
+// stream and the workspace slots belong to ctx->device, whatever device the
+// calling thread has current.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+#define CTX_GUARD(ctx)                          \
+  if (!(ctx)) return KST_ERR_DIMENSION;         \
+  DeviceGuard guard__((ctx)->device);           \
+  (ctx)->err.clear();
+
 void* ws_get(kst_ctx* ctx, int slot, size_t bytes);  // may return nullptr on OOM
 void* pinned_get(kst_ctx* ctx, size_t bytes);
 // Upload `bytes` of host data to a __constant__ `symbol` on the current

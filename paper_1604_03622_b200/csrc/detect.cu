@@ -476,8 +476,9 @@ __global__ void __launch_bounds__(NT, KST_CB_MINB) combine_kernel(
   for (int e = threadIdx.x; e < a.G * P; e += NT) s_h[e] = hconj[e];
   const int d = blockIdx.x * NT + threadIdx.x;
   const int per = a.G / a.groups;
-  const int64_t m_end = min((int64_t)(blockIdx.y + 1) * CB_BINS, n);
-  for (int64_t m = (int64_t)blockIdx.y * CB_BINS; m < m_end; ++m) {
+  // bin blocks stride over gridDim.y (capped at 65535 by the launch)
+  for (int64_t mb = blockIdx.y; mb * CB_BINS < n; mb += gridDim.y)
+  for (int64_t m = mb * CB_BINS, m_end = min((mb + 1) * CB_BINS, n); m < m_end; ++m) {
     __syncthreads();  // previous bin's s_c fully consumed
     if (a.mode != 2) {
       for (int e = threadIdx.x; e < P * a.kb; e += NT) s_c[e] = coef[m * P * a.kb + e];
@@ -588,16 +589,18 @@ __global__ void __launch_bounds__(NT) coef_kernel(const cplx* __restrict__ src, 
 __global__ void __launch_bounds__(NT) filter_apply_kernel(
     const cplx* __restrict__ cube, const cplx* __restrict__ coef, const cplx* __restrict__ ub,
     const cplx* __restrict__ ua, int P, int q, int ka, int kb, int mode, int spatial,
-    cplx* __restrict__ out) {
+    cplx* __restrict__ out, int64_t n) {
   __shared__ cplx s_ua[kMaxP * kMaxP];
   __shared__ cplx s_c[kMaxP * kMaxKB];
-  const int64_t m = blockIdx.y;
+  __shared__ cplx s_e[kMaxP * kMaxKB];
   for (int e = threadIdx.x; e < P * ka; e += NT) s_ua[e] = ua[e];
+  // bins stride over gridDim.y (capped at 65535 by the launch)
+  for (int64_t m = blockIdx.y; m < n; m += gridDim.y) {
+  __syncthreads();  // previous bin's s_c consumed
   if (mode != 2)
     for (int e = threadIdx.x; e < P * kb; e += NT) s_c[e] = coef[m * P * kb + e];
   __syncthreads();
   if (mode == 1) {
-    __shared__ cplx s_e[kMaxP * kMaxKB];
     for (int e = threadIdx.x; e < P * kb; e += NT) {
       const int i = e / kb, k = e % kb;
       cplx acc = cmk(0, 0);
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(NT) filter_apply_kernel(
     __syncthreads();
   }
   const int t = blockIdx.x * NT + threadIdx.x;
-  if (t >= q) return;
+  if (t >= q) continue;
   cplx y[kMaxP];
 #pragma unroll
   for (int i = 0; i < kMaxP; ++i)
@@ -640,6 +643,7 @@ __global__ void __launch_bounds__(NT) filter_apply_kernel(
 #pragma unroll
   for (int i = 0; i < kMaxP; ++i)
     if (i < P) out[(m * P + i) * q + t] = y[i];
+  }
 }
 
 #define KST_DISPATCH_P4(P, ...)                           \
@@ -1249,7 +1253,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   a.mode = mode;
   a.spatial = spatial;
   a.inv_sqrt_q = 1.0 / sqrt((double)q);
-  KST_DISPATCH_P(p, (combine_kernel<PP><<<dim3(cdiv(D, NT), cdiv(n, CB_BINS)), NT,
+  KST_DISPATCH_P(p, (combine_kernel<PP><<<dim3(cdiv(D, NT), (unsigned)std::min<int64_t>(cdiv(n, CB_BINS), 65535)), NT,
                                           sizeof(cplx) * G * p, st>>>(
                         spec, coef, ubspec, has_a ? ua : hconj, hconj, a, values, n)));
   KST_LAUNCH(ctx);
@@ -1281,8 +1285,8 @@ int filter_cube(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const c
   KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));
   coef_kernel<<<(unsigned)rows, NT, 0, st>>>(cube, q, ub, kb_used, coef, flag);
   KST_LAUNCH(ctx);
-  filter_apply_kernel<<<dim3(cdiv(q, NT), (unsigned)n), NT, 0, st>>>(
-      cube, coef, ub, has_a ? ua : coef, p, q, has_a ? ka : 0, kb_used, mode, spatial, out);
+  filter_apply_kernel<<<dim3(cdiv(q, NT), (unsigned)std::min<int64_t>(n, 65535)), NT, 0, st>>>(
+      cube, coef, ub, has_a ? ua : coef, p, q, has_a ? ka : 0, kb_used, mode, spatial, out, n);
   KST_LAUNCH(ctx);
   int hflag = 0;
   KST_CUDA(ctx, cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1296,15 +1300,14 @@ int filter_cube(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const c
 extern "C" int kst_filter(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
                           const double* ua, int ka, const double* ub, int kb, int kind,
                           int spatial_only, double* out, void* stream) {
-  if (!ctx) return KST_ERR_DIMENSION;
-  ctx->err.clear();
+  CTX_GUARD(ctx);
   return kst::filter_cube(ctx, (const cplx*)cube, n, p, q, (const cplx*)ua, ka, (const cplx*)ub, kb,
                           kind, spatial_only, (cplx*)out, (cudaStream_t)stream);
 }
 
 extern "C" int kst_change(kst_ctx* ctx, const double* a, const double* b, int64_t count,
                           int is_signed, double* out, void* stream) {
-  if (!ctx) return KST_ERR_DIMENSION;
+  CTX_GUARD(ctx);
   if (count <= 0) return KST_OK;
   change_kernel<<<cdiv(count, 256) > 4096 ? 4096 : cdiv(count, 256), 256, 0, (cudaStream_t)stream>>>(
       a, b, count, is_signed, out);

@@ -920,37 +920,40 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   const size_t stat_stride = STAT_STRIDE;
   const int nvx = (q + V_ROWS - 1) / V_ROWS;
   const int nbb = (q + NT - 1) / NT;
+  // M path: small P, valid ranks, no per-iteration b copies requested
+  static const bool mpath_env = !(getenv("KST_LRKRON_MPATH") && atoi(getenv("KST_LRKRON_MPATH")) == 0);
+  const bool mpath = mpath_env && p <= 4 && !iter_b && !iter_spatial && ra >= 1 && ra <= p &&
+                     rb >= 1 && rb <= q && max_iter >= 1;
+  // P = 3: one wave of pipelined CTAs (rows_per rows each); others MG_ROWS rows
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int rows_per = p == 3 ? (q + nsm - 1) / nsm : MG_ROWS;
+  const int nblk = (q + rows_per - 1) / rows_per;
+  size_t rec = 0;
+  KST_DISPATCH_P(p, (rec = MDims<PP>::STRIDE));
+  // WS_PART is taken ONCE, sized for every use below (stats / V / b partials and
+  // the M-path records): a second ws_get on a grown slot would free the buffer
+  // the b-step partials still point into.
+  size_t part_bytes = std::max(sizeof(double) * stat_stride * p * nbx,
+                               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64);
+  if (mpath) part_bytes = std::max(part_bytes, sizeof(double) * rec * nblk + 64);
   char* small = (char*)ws_get(ctx, WS_SMALL, sizeof(IterState) + 256);
-  double* part = (double*)ws_get(
-      ctx, WS_PART,
-      std::max(sizeof(double) * stat_stride * p * nbx,
-               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64));
+  double* part = (double*)ws_get(ctx, WS_PART, part_bytes);
   cplx* b = (cplx*)ws_get(ctx, WS_B, sizeof(cplx) * (size_t)q * q);
   // one pinned staging buffer: [0, 64) small scalars, [64, ...) M-path residuals
   double* hbuf = (double*)pinned_get(ctx, sizeof(double) * (64 + std::max(max_iter, 1) + 32));
   if (!small || !part || !b || !hbuf) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");
   IterState* state = (IterState*)small;
 
-  // M path: small P, valid ranks, no per-iteration b copies requested
-  static const bool mpath_env = !(getenv("KST_LRKRON_MPATH") && atoi(getenv("KST_LRKRON_MPATH")) == 0);
-  const bool mpath = mpath_env && p <= 4 && !iter_b && !iter_spatial && ra >= 1 && ra <= p &&
-                     rb >= 1 && rb <= q && max_iter >= 1;
   double* mres = nullptr;
   double* minfo = nullptr;
   if (mpath) {
-    // P = 3: one wave of pipelined CTAs (rows_per rows each); others MG_ROWS rows
-    static int nsm = 0;
-    if (!nsm) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      if (nsm <= 0) nsm = 148;
-    }
-    const int rows_per = p == 3 ? (q + nsm - 1) / nsm : MG_ROWS;
-    const int nblk = (q + rows_per - 1) / rows_per;
-    size_t rec = 0;
-    KST_DISPATCH_P(p, (rec = MDims<PP>::STRIDE));
-    double* mpart = (double*)ws_get(ctx, WS_PART, sizeof(double) * rec * nblk + 64);
+    double* mpart = part;  // consumed by m_iterate_kernel before bstep reuses the slot (same stream)
     double* dres = (double*)ws_get(ctx, WS_VALS, sizeof(double) * (max_iter + 8));
     mres = hbuf ? hbuf + 64 : nullptr;
     if (!mpart || !dres || !mres) return set_err(ctx, KST_ERR_CUDA, "lrkron: workspace");

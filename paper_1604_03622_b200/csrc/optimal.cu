@@ -101,8 +101,7 @@ __global__ void finite_kernel(const cplx* __restrict__ x, int64_t count, int* __
 }  // namespace
 
 extern "C" int kst_chol(kst_ctx* ctx, const double* sigma, int d, double* L, void* stream) {
-  if (!ctx) return KST_ERR_DIMENSION;
-  ctx->err.clear();
+  CTX_GUARD(ctx);
   if (d < 1) return set_err(ctx, KST_ERR_DIMENSION, "chol: dimension %d", d);
   if ((const void*)sigma == (const void*)L)  // the tiled transpose cannot run in place
     return set_err(ctx, KST_ERR_DIMENSION, "chol: L must not alias sigma");
@@ -139,8 +138,7 @@ extern "C" int kst_chol(kst_ctx* ctx, const double* sigma, int d, double* L, voi
 
 extern "C" int kst_chol_solve(kst_ctx* ctx, const double* L, int d, const double* B, int64_t nrhs,
                               double* X, void* stream) {
-  if (!ctx) return KST_ERR_DIMENSION;
-  ctx->err.clear();
+  CTX_GUARD(ctx);
   if (d < 1 || nrhs < 0 || nrhs > 0x7fffffff)
     return set_err(ctx, KST_ERR_DIMENSION, "chol_solve: d=%d nrhs=%lld", d, (long long)nrhs);
   if (nrhs == 0) return KST_OK;

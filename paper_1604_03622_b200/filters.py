@@ -154,6 +154,7 @@ def build_filter(kind, estimate=None, sigma=None, p=None, q=None, drop_temporal=
     sp = estimate._sp.dev() if hasattr(estimate, "_sp") else nat.to_device(estimate.spatial)
     ua = subspace_basis_device(sp, estimate.rank_spatial, rank_tol)
     tb = getattr(estimate, "_tb", None)
+    tp = None
     if tb is not None:
         vecs, vals = tb
         keep = 0
@@ -164,9 +165,7 @@ def build_filter(kind, estimate=None, sigma=None, p=None, q=None, drop_temporal=
     else:
         tp = estimate._tp.dev() if hasattr(estimate, "_tp") else nat.to_device(estimate.temporal)
         ub = subspace_basis_device(tp, estimate.rank_temporal, rank_tol)
-    p_, q_ = sp.shape[0], (tb[0].shape[0] if tb is not None else
-                           (estimate._tp.dev().shape[0] if hasattr(estimate, "_tp")
-                            else np.shape(estimate.temporal)[0]))
+    p_, q_ = sp.shape[0], (tb[0].shape[0] if tb is not None else tp.shape[0])
     f = StapFilter(kind, p_, q_,
                    None if ua is None else Dual.from_device(ua, device_mode),
                    None if ub is None else Dual.from_device(ub, device_mode),

@@ -9,6 +9,7 @@ same way for the CPU tests). One process per GPU, launched by torchrun.
 
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -66,8 +67,20 @@ def process_sequence(frames, rank_spatial=1, rank_temporal=3, dopplers=None, spa
         return maps
     dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
         else torch.device("cpu")
-    local = torch.stack([m.to(dev) for m in maps]) if maps else torch.zeros((0,), device=dev)
+    local = local_stack(maps, frames, dopplers, dev)
     return gather_maps(local, len(frames), group)
+
+
+def local_stack(maps, frames, dopplers, dev):
+    """This rank's maps as one (k_local, n, D) tensor on `dev`. A rank with no
+    frames (fewer frames than ranks) contributes an EMPTY stack of the same
+    trailing shape, so all_gather sees equal (per, n, D) pads on every rank."""
+    if maps:
+        return torch.stack([torch.as_tensor(m).to(dev) for m in maps])
+    n_bins = int(frames[0].shape[0]) if len(frames) else 0
+    n_dop = (len(np.ravel(dopplers)) if dopplers is not None
+             else (int(frames[0].shape[2]) if len(frames) else 0))
+    return torch.zeros((0, n_bins, n_dop), dtype=torch.float64, device=dev)
 
 
 # ----------------------------------------------------------------- L-mode tiles

@@ -45,6 +45,39 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _few_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import kron_oracle as orc
+        frames = _frames()[:1]  # one frame, two ranks: rank 1 holds nothing
+        mine = parallel.local_frames(len(frames), rank, world)
+        maps = [orc.pipeline(frames[f], 1, 3, 16)[3] for f in mine]
+        local = parallel.local_stack(maps, frames, np.arange(16) / 16, torch.device("cpu"))
+        full = parallel.gather_maps(local, len(frames))
+        want = orc.pipeline(frames[0], 1, 3, 16)[3][None]
+        q.put((rank, tuple(local.shape), bool(np.array_equal(full.numpy(), want))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_fewer_frames_than_ranks_gathers_equal_shapes():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_few_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    res = {r: rest for r, *rest in res}
+    assert res[0][0] == (1, 24, 16) and res[1][0] == (0, 24, 16)
+    assert res[0][1] and res[1][1]
+
+
 def test_frame_assignment_is_a_partition():
     for n, w in ((0, 1), (5, 2), (100, 8), (3, 4)):
         parts = parallel.frame_assignment(n, w)

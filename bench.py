@@ -28,6 +28,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# arithmetic of the path: c128 cube in, f64 map out; K1 (sample covariance)
+# on the int8 tensor cores as an exact CRT integer Gram of the columns rounded
+# to 32-bit significands (K1); K2-K5 in FP64
+DTYPE = "f64 (K1: int8 CRT Gram of 32-bit-rounded columns)"
+
 CONFIGS = {
     # name: (p, q, n_bins, D, G, ra, rb, K passes)
     "gotcha": (3, 2001, 2001, 2001, 16, 1, 3, 1),
@@ -44,6 +49,10 @@ def parse():
     ap.add_argument("--config", default="gotcha",
                     choices=sorted(CONFIGS) + ["lmode", "multipass", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # internal: one threading mode of the reference arm (time_reference)
+    ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--ref-threads", type=int, default=1, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-steps", type=int, default=3, help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -178,15 +187,32 @@ def int8_roofline(ops, gemm_ms, slices, flops, gram_ms):
                            "dense on B200); cuBLAS int8 measured 3.03 POPS here (tools/int8_probe.py)"}
 
 
+def int8_peak():
+    """Measured dense int8 peak (profiles/r02_int8_peak.json, tools/int8_peak.py:
+    cuBLASLt int8 8192^3 on this pool's B200, burst = best of 10 and sustained =
+    4 s back to back). The bench's timed region is ~60 ms, so the BURST figure
+    is the roofline denominator (B200_PROFILING.md: burst for a kernel timed
+    alone or in a short region). Fallback: 2 x the measured bf16 burst."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_int8_peak.json")) as f:
+            d = json.load(f)
+        return (d["int8_dense_tops_burst"], d["int8_dense_tops_sustained"],
+                "measured: cuBLASLt int8 8192^3 burst (best of 10), profiles/r02_int8_peak.json")
+    except (OSError, ValueError, KeyError):
+        pk = measured_peaks()
+        b = 2.0 * pk.get("bf16_tflops", 1629.7)
+        return b, 2.0 * pk.get("bf16_tflops_sustained", 1376.6), \
+            "fallback: 2 x MEASURED_PEAKS.json bf16_tflops (burst)"
+
+
 def crt_roofline(nmod, n, d, tc_ms, executed_ops, flops, gram_ms):
     """Dominant kernel of the CRT engine: gram_tc_kernel (hand-written tcgen05,
     int8 tensor cores). Algorithmic work: per modulus four real int8 products
     (Re: XrXr + XiXi, Im: XiXr - XrXi) for each of the n d (d + 1) / 2 Hermitian
     entries, 2 ops per MAC. Duration: CUDA events bracketing that one launch
-    (kst_stage_times entry 5). Peak: 2 x the measured dense bf16 rate in
-    MEASURED_PEAKS.json (int8 dense = 2 x bf16 dense on B200)."""
-    pk = measured_peaks()
-    peak = 2.0 * pk.get("bf16_tflops_sustained", 1376.6)
+    (kst_stage_times entry 5). Peak: the measured dense int8 rate in
+    profiles/r02_int8_peak.json (burst; the sustained fraction is reported too)."""
+    peak, peak_sus, peak_src = int8_peak()
     alg = 2.0 * 4.0 * nmod * n * d * (d + 1) / 2.0
     traffic, _ = ncu_traffic("gram_tc_ncu.json")
     achieved = alg / (tc_ms * 1e-3) / 1e12 if tc_ms > 0 else 0.0
@@ -196,9 +222,9 @@ def crt_roofline(nmod, n, d, tc_ms, executed_ops, flops, gram_ms):
             "algorithmic": f"8*nmod*n*d(d+1)/2 = {alg:.4e} int8 ops per launch "
                            f"({executed_ops:.4e} issued incl. 128-tile padding)",
             "kernel_ms": tc_ms, "gram_stage_ms": gram_ms,
+            "frac_of_sustained_peak": achieved / peak_sus, "peak_sustained": peak_sus,
             "fp64_equivalent_tflops": flops / (gram_ms * 1e-3) / 1e12,
-            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops_sustained (int8 dense = 2 x bf16 "
-                           "dense on B200)"}
+            "peak_source": peak_src}
 
 
 def cpu_threads():
@@ -214,29 +240,131 @@ def oracle_frame(cube, cfg):
 
 
 # ----------------------------------------------------------------- reference arm
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def host_info():
+    """CPU model, core count, numpy and BLAS vendor/version of this host."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        import threadpoolctl
+        info = [x for x in threadpoolctl.threadpool_info() if x.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')} ({info[0].get('architecture')})"
+    except Exception:
+        pass
+    return {"cpu_model": model, "cores": cpu_threads(), "numpy": np.__version__, "blas": blas}
+
+
+def ref_worker(args):
+    """One threading mode of the reference arm, in its own process so the BLAS
+    thread count is fixed before numpy loads (env set by the parent). Runs the
+    UNMODIFIED reference package installed in baseline/_ref through its public
+    API -- the README library sequence (pkg/README.md:144-161):
+    sample_covariance -> lr_kron_estimate -> build_filter -> detection_image,
+    with WorkerPool(threads) -- on the bench frame; one untimed warm-up on a
+    small frame, then `steps` timed frames (perf_counter). Prints one JSON."""
+    sys.path.insert(0, REF_DIR)
+    import kronstap
+    from kronstap.layout import cube_to_snapshots
+    assert os.path.dirname(kronstap.__file__).startswith(REF_DIR), kronstap.__file__
+    cfg = CONFIGS[args.config]
+    p, q, n, D, G, ra, rb, K = cfg
+    cube = make_frame(cfg, 17)
+    dop, grid = kronstap.make_doppler_grid(D), kronstap.make_spatial_grid(p, G)
+
+    def frame(c, pool, dd):
+        scm = kronstap.sample_covariance(cube_to_snapshots(c), p, c.shape[2], pool=pool)
+        est = kronstap.lr_kron_estimate(scm, ra, rb, pool=pool)
+        filt = kronstap.build_filter("kron", estimate=est)
+        return kronstap.detection_image(filt, c, dd, grid, pool=pool).values
+
+    with kronstap.WorkerPool(args.ref_threads) as pool:
+        small = np.ascontiguousarray(cube[:96, :, :64])
+        frame(small, pool, kronstap.make_doppler_grid(64))  # warm-up (BLAS threads, page-in)
+        times = []
+        for _ in range(args.ref_steps):
+            t0 = time.perf_counter()
+            vals = frame(cube, pool, dop)
+            times.append(time.perf_counter() - t0)
+    print(json.dumps({"times": times, "map_sum": float(vals.sum()),
+                      "kronstap": os.path.dirname(kronstap.__file__)}), flush=True)
+
+
+def time_reference(args, steps, modes=("blas", "pool")):
+    """Time the reference on this host in the SURVEY.md §8(d) threading modes:
+    "blas" = OPENBLAS_NUM_THREADS=N with WorkerPool(1); "pool" =
+    OPENBLAS_NUM_THREADS=1 with WorkerPool(N) (src/parallel.py:34-68). Each
+    mode runs in a subprocess. Returns {mode: median seconds per frame} and
+    the per-mode records, or None when baseline/_ref is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "kronstap")):
+        return None
+    ncore = cpu_threads()
+    out = {}
+    for mode in modes:
+        env = dict(os.environ)
+        blas_t, pool_t = (ncore, 1) if mode == "blas" else (1, ncore)
+        for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+            env[k] = str(blas_t)
+        env.pop("RANK", None), env.pop("WORLD_SIZE", None), env.pop("LOCAL_RANK", None)
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", args.config, "--ref-worker",
+               "--ref-threads", str(pool_t), "--ref-steps", str(steps)]
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1800)
+        if r.returncode != 0:
+            out[mode] = {"error": r.stderr.strip().splitlines()[-1:] if r.stderr else "rc != 0"}
+            continue
+        rec = json.loads(r.stdout.strip().splitlines()[-1])
+        rec["median_s"] = statistics.median(rec["times"])
+        rec["blas_threads"], rec["pool_threads"] = blas_t, pool_t
+        out[mode] = rec
+    return out
+
+
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    cube = make_frame(cfg, 17)
     p, q, n, D, G, ra, rb, K = cfg
     px = n * D
-    # bounded sample: each step is one full frame through the CPU port of the
-    # reference path; the step count is capped so the run stays within minutes
-    ksteps, wsteps = min(args.steps, 3), min(args.warmup, 1)
-    for _ in range(wsteps):
-        oracle_frame(cube, cfg)
-    times = [oracle_frame(cube, cfg)[0] for _ in range(ksteps)]
-    total = sum(times)
-    value = px * ksteps / total
+    # bounded sample: each timed step is one full frame through the reference;
+    # at most 3 timed frames per threading mode so the arm ends within minutes
+    ksteps = max(1, min(args.steps, 3))
+    modes = time_reference(args, ksteps)
+    if modes and any("median_s" in m for m in modes.values()):
+        ok = {k: v for k, v in modes.items() if "median_s" in v}
+        best = min(ok, key=lambda k: ok[k]["median_s"])
+        secs = ok[best]["median_s"]
+        kind = "reference"
+        sample = (f"median of {ksteps} full frames per threading mode through the unmodified "
+                  f"reference (baseline/_ref/kronstap, README library sequence); faster mode "
+                  f"'{best}' reported")
+        cores = ok[best]["blas_threads"] * ok[best]["pool_threads"]
+        detail = {k: {kk: v[kk] for kk in ("median_s", "times", "blas_threads", "pool_threads")
+                      if kk in v} if "median_s" in v else v for k, v in modes.items()}
+    else:
+        # reference not installed: the numpy restatement (oracle port)
+        cube = make_frame(cfg, 17)
+        oracle_frame(np.ascontiguousarray(cube[:64, :, :64]), (p, 64, 64, 64, G, ra, rb, K))
+        ts = [oracle_frame(cube, cfg)[0] for _ in range(ksteps)]
+        secs, kind, cores, detail = statistics.median(ts), "port", cpu_threads(), None
+        sample = f"median of {ksteps} full frames through oracle/kron_oracle.pipeline"
+    value = px / secs
     line = {
         "impl": "reference", "metric": "STAP pixels/sec", "value": value, "unit": "pixels/s",
-        "n_gpus": args.gpus, "steps": ksteps, "steps_requested": args.steps, "warmup": wsteps,
-        "ms_per_step": 1e3 * total / ksteps, "higher_is_better": True, "scaling": "weak",
+        "n_gpus": args.gpus, "steps": ksteps, "steps_requested": args.steps, "warmup": 1,
+        "ms_per_step": 1e3 * secs, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic (reference simulator, seed 17)",
         "config": config_block(args, cfg, world),
-        "cpu_baseline": {"value": value, "unit": "pixels/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": f"{ksteps} full frame(s) through oracle/kron_oracle.pipeline "
-                                   "(numpy restatement of the reference path; BLAS on all host threads)"},
+        "cpu_baseline": {"value": value, "unit": "pixels/s", "cores": cores, "kind": kind,
+                         "sample": sample, "modes": detail, "host": host_info()},
         "e2e": {"value": value, "unit": "pixels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -318,7 +446,7 @@ def run_lmode(args, rank, local, world):
     print(json.dumps({
         "metric": "STAP pixels/sec", "value": px / (ms / 1e3), "unit": "pixels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic (reference simulator restated in scenes.py; seeded, 8 movers)",
         "config": {"workload": f"configs[3] L-mode: {nb} bins x {D} Doppler x {G} spatial, p={p} "
                                f"q={q}, n_w={n_w} training bins per test bin "
@@ -389,7 +517,7 @@ def run_sweep(args, rank, local, world):
             "metric": "STAP pixels/sec", "value": px / (tot_ms / 1e3), "unit": "pixels/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128/f64",
+            "vs_baseline": None, "dtype": DTYPE,
             "data": "synthetic (reference simulator restated in scenes.py; seeded, 8 movers)",
             "config": {"workload": "configs[3] sweep: L-mode n_w in {9,25,49,81} + global, ranks "
                                    "(r_a, r_b) in {1,2,3}^2, 256 x 256 frame, 256 Doppler x 16 "
@@ -484,7 +612,7 @@ def run_multipass(args, rank, local, world):
         "metric": "STAP pass-pixels/sec", "value": px / (ms / 1e3), "unit": "pixels/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128/f64",
+        "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic (reference simulator restated in scenes.py; 4 passes, seeded, 8 movers)",
         "config": {"workload": f"configs[4] multipass: K={K} passes x {n} bins x {D} Doppler, "
                                f"p={p} (stacked {K * p}) q={q}, ranks ({K}, {rb}), "
@@ -500,6 +628,9 @@ def run_multipass(args, rank, local, world):
 
 def main():
     args = parse()
+    if args.ref_worker:
+        ref_worker(args)
+        return
     if args.config == "sweep" and args.impl == "ours":
         run_sweep(args, *dist_env())
         return
@@ -519,6 +650,9 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
+        # communicator logging (rank count visible to the driver)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     import paper_1604_03622_b200 as kst
     from paper_1604_03622_b200 import _native as nat
@@ -583,7 +717,10 @@ def main():
     torch.cuda.synchronize(dev)
     h2d_ms = h0.elapsed_time(h1)
     del probe
-    fs = FrameStream((n, p, q), dev, ra, rb, dop, grid)
+    # N > 1: every step's maps are all-gathered over NCCL (NVLink) and rank 0
+    # downloads the gathered stack -- the map gather is inside the e2e region
+    fs = FrameStream((n, p, q), dev, ra, rb, dop, grid,
+                     gather_group=dist.group.WORLD if world > 1 else None)
     for i in range(args.warmup):
         fs.submit(pinned[i % 2])
     last = fs.flush()
@@ -628,7 +765,7 @@ def main():
         line = {
             "metric": "STAP pixels/sec", "value": value, "unit": "pixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128/f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
             "data": "synthetic (reference simulator restated in scenes.py; seeded SIRV clutter + 8 movers)",
             "config": config_block(args, cfg, world),
             "stages_ms": {"scm": gram_ms, "lrkron": float(st[1]), "bases": float(st[2]),
@@ -638,24 +775,40 @@ def main():
             "roofline": roof,
             "e2e": {"value": e2e_value, "unit": "pixels/s",
                     "h2d_bytes_per_step": int(host_cubes[0].nbytes),
-                    "d2h_bytes_per_step": int(n * D * 8),
+                    "d2h_bytes_per_step": int(world * n * D * 8),
+                    "nccl_gather_bytes_per_step": int((world - 1) * world * n * D * 8)
+                    if world > 1 else 0,
                     "h2d_ms_per_cube": h2d_ms,
                     "h2d_gbps": host_cubes[0].nbytes / (h2d_ms * 1e-3) / 1e9,
                     "pcie_bound_pixels_per_s": px_step / (h2d_ms * 1e-3),
                     "note": "upload, compute and download overlap (FrameStream); the e2e "
-                            "rate is bounded by the host->device copy of each 192 MB cube"},
+                            "rate is bounded by the host->device copy of each 192 MB cube"
+                            + ("; N > 1: each step's maps all-gathered over NCCL and the "
+                               "gathered stack read back by rank 0" if world > 1 else "")},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            oracle_frame(host_cubes[0][:64, :, :64].copy(), (p, 64, 64, 64, G, ra, rb, K))  # BLAS warm-up
-            secs, ref_vals = oracle_frame(host_cubes[0], cfg)
-            got = out[0].cpu().numpy()  # last step processed cubes[(steps-1) % 2]
-            line["cpu_baseline"] = {
-                "value": n * D / secs, "unit": "pixels/s", "cores": cpu_threads(), "kind": "port",
-                "sample": "1 full frame through oracle/kron_oracle.pipeline (numpy restatement of "
-                          "the reference path, BLAS on all host threads)"}
-            del got, ref_vals
+            # bounded sample: the unmodified reference (baseline/_ref) in its
+            # faster threading mode (BLAS threads), median of 2 full frames
+            modes = time_reference(args, 2, modes=("blas",))
+            if modes and "median_s" in modes.get("blas", {}):
+                m = modes["blas"]
+                line["cpu_baseline"] = {
+                    "value": n * D / m["median_s"], "unit": "pixels/s",
+                    "cores": m["blas_threads"] * m["pool_threads"], "kind": "reference",
+                    "sample": "median of 2 full frames through the unmodified reference "
+                              "(baseline/_ref/kronstap, README library sequence, "
+                              "OPENBLAS_NUM_THREADS = all host cores, WorkerPool(1))",
+                    "host": host_info()}
+            else:
+                secs, _ = oracle_frame(host_cubes[0], cfg)
+                line["cpu_baseline"] = {
+                    "value": n * D / secs, "unit": "pixels/s", "cores": cpu_threads(),
+                    "kind": "port",
+                    "sample": "1 full frame through oracle/kron_oracle.pipeline (numpy "
+                              "restatement of the reference path, BLAS on all host threads)",
+                    "host": host_info()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

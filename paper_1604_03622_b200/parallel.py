@@ -52,23 +52,77 @@ def gather_maps(local_maps, n_frames, group=None, dst_all=True):
 
 
 def process_sequence(frames, rank_spatial=1, rank_temporal=3, dopplers=None, spatial_grid=None,
-                     group=None, gather=True, **kw):
-    """Run the fused pipeline over this rank's share of `frames` (a list of
-    (n, p, q) cubes, numpy or CUDA) and optionally gather all maps."""
-    from .pipeline import process_frame
+                     group=None, gather=True, tol=1e-4, max_iter=100, kind="kron", device=None):
+    """Run the fused pipeline over this rank's share of `frames` (a sequence
+    of (n, p, q) cubes: numpy, CPU tensors -- pinned or not -- or CUDA
+    tensors) and optionally all-gather every rank's maps.
+
+    Uploads overlap compute: frame j+1 is staged into a pinned host buffer
+    and copied host -> device on a side stream while frame j runs on the
+    compute stream (two device cube buffers, event-ordered). Maps are written
+    straight into one device stack (k_local, n, D), which is what the NCCL
+    all-gather sends -- no device -> host -> device round trip.
+    Returns the (n_frames, n, D) float64 tensor on this rank's device
+    (gather and world > 1), else this rank's (k_local, n, D) stack.
+    """
+    from . import _native as nat
+    from .pipeline import process_frame_device
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     mine = local_frames(len(frames), rank, world)
-    maps = []
-    for f in mine:
-        vals, _ = process_frame(frames[f], rank_spatial, rank_temporal, dopplers, spatial_grid, **kw)
-        maps.append(torch.as_tensor(vals))
+    dev = torch.device("cuda", nat.device_index(device))
+    if len(frames):
+        n, p, q = (int(s) for s in frames[0].shape)
+    else:
+        n = p = q = 0
+    D = len(np.ravel(dopplers)) if dopplers is not None else q
+    maps = torch.empty((len(mine), n, D), dtype=torch.float64, device=dev)
+    if mine:
+        comp = torch.cuda.current_stream(dev)
+        up = torch.cuda.Stream(dev)
+        bufs = [torch.empty((n, p, q), dtype=torch.complex128, device=dev) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        done = [torch.cuda.Event() for _ in range(2)]
+        staged = [None, None]
+        pins, pin_free = [None, None], [torch.cuda.Event() for _ in range(2)]
+
+        def upload(j):
+            slot = j % 2
+            src = frames[mine[j]]
+            if isinstance(src, torch.Tensor) and src.is_cuda:
+                staged[slot] = src  # already resident: no copy
+                ready[slot].record(comp)
+                return
+            if isinstance(src, torch.Tensor) and src.is_pinned():
+                host = src
+            else:
+                if pins[slot] is None:
+                    pins[slot] = torch.empty((n, p, q), dtype=torch.complex128).pin_memory()
+                pin_free[slot].synchronize()  # previous upload out of this pin buffer done
+                pins[slot].copy_(torch.as_tensor(np.asarray(src, dtype=np.complex128))
+                                 if not isinstance(src, torch.Tensor) else src)
+                host = pins[slot]
+            with torch.cuda.stream(up):
+                up.wait_event(done[slot])  # device buffer free once frame j-2 finished
+                bufs[slot].copy_(host, non_blocking=True)
+                ready[slot].record(up)
+                pin_free[slot].record(up)
+            staged[slot] = bufs[slot]
+
+        upload(0)
+        for j in range(len(mine)):
+            if j + 1 < len(mine):
+                upload(j + 1)
+            slot = j % 2
+            comp.wait_event(ready[slot])
+            process_frame_device(staged[slot], rank_spatial, rank_temporal, dopplers, spatial_grid,
+                                 tol, max_iter, kind, out=maps[j:j + 1])
+            done[slot].record(comp)
     if not gather or world == 1:
         return maps
-    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" \
-        else torch.device("cpu")
-    local = local_stack(maps, frames, dopplers, dev)
-    return gather_maps(local, len(frames), group)
+    if dist.get_backend(group) != "nccl":
+        maps = maps.cpu()
+    return gather_maps(maps, len(frames), group)
 
 
 def local_stack(maps, frames, dopplers, dev):

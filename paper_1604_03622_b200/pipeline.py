@@ -72,7 +72,7 @@ class FrameStream:
 
     def __init__(self, shape, device=None, rank_spatial=1, rank_temporal=3, dopplers=None,
                  spatial_grid=None, tol=1e-4, max_iter=100, kind="kron", out_pinned=None, nbuf=3,
-                 groups=1):
+                 groups=1, gather_group=None):
         import torch
         self.dev = torch.device("cuda", nat.device_index(device))
         n, p, q = shape
@@ -87,6 +87,20 @@ class FrameStream:
         self.outs = [torch.empty((groups, n, D), dtype=torch.float64, device=self.dev)
                      for _ in range(nbuf)]
         hshape = (n, D) if groups == 1 else (groups, n, D)
+        # gather_group (torch.distributed, NCCL): every frame's maps are
+        # all-gathered over NVLink into a (world, groups, n, D) device stack
+        # right after the frame, and rank 0 downloads the whole gathered
+        # stack (the other ranks download nothing): the SURVEY.md §8e map
+        # gather inside the end-to-end stream
+        self.gather = gather_group
+        self.rank0 = True
+        if gather_group is not None:
+            import torch.distributed as dist
+            self.world = dist.get_world_size(gather_group)
+            self.rank0 = dist.get_rank(gather_group) == 0
+            self.gbufs = [torch.empty((self.world, groups, n, D), dtype=torch.float64,
+                                      device=self.dev) for _ in range(nbuf)]
+            hshape = (self.world,) + ((n, D) if groups == 1 else (groups, n, D))
         self.host_out = out_pinned if out_pinned is not None else [
             torch.empty(hshape, dtype=torch.float64).pin_memory() for _ in range(nbuf)]
         if len(self.host_out) < nbuf:
@@ -126,11 +140,20 @@ class FrameStream:
         self.comp.wait_event(self.ready[slot])
         self.comp.wait_event(self.back[slot])  # map buffer read back (frame i - nbuf)
         process_frame_device(self.bufs[slot], *self.args, out=self.outs[slot], summary=self.summary)
+        if self.gather is not None:
+            import torch.distributed as dist
+            # NCCL all-gather on its own stream, ordered after this frame; the
+            # compute stream waits for it before reusing gbufs/outs
+            dist.all_gather_into_tensor(self.gbufs[slot], self.outs[slot], group=self.gather)
         self.done[slot].record(self.comp)
         with torch.cuda.stream(self.copy_back):
             self.copy_back.wait_event(self.done[slot])
-            src = self.outs[slot][0] if self.groups == 1 else self.outs[slot]
-            self.host_out[slot].copy_(src, non_blocking=True)
+            if self.gather is None:
+                src = self.outs[slot][0] if self.groups == 1 else self.outs[slot]
+                self.host_out[slot].copy_(src, non_blocking=True)
+            elif self.rank0:
+                src = self.gbufs[slot][:, 0] if self.groups == 1 else self.gbufs[slot]
+                self.host_out[slot].copy_(src, non_blocking=True)
             self.back[slot].record(self.copy_back)
         self.pending = None
         return self.host_out[slot], self.back[slot]

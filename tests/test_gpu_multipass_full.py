@@ -1,8 +1,8 @@
 """configs[4] (SURVEY.md §8 cfg 5): 4-pass 3-channel stacks through the fused
-pipeline (kst_pipeline, groups = K) -- against the oracle at a mid size where
-the CPU restatement finishes in seconds, and at the full 2001 x 2001 size
-against the unfused device API chain (multipass_estimate -> build_filter ->
-pass_images), which runs the same numerics through separate C calls."""
+pipeline (kst_pipeline, groups = K) -- against the oracle at mid sizes where
+the CPU restatement finishes in seconds. The full 2001 x 2001 stack is
+checked against the unmodified reference's own outputs in
+tests/test_gpu_fullsize_ref.py."""
 
 import numpy as np
 import pytest
@@ -42,18 +42,3 @@ def test_fused_multipass_matches_oracle(q):
     m0 = orc.detect("kron", None, None, st, orc.doppler_grid(q), orc.spatial_grid(K * P, G)).max()
     got = vals.cpu().numpy()
     assert np.all(np.abs(got - want) <= map_tolerance(want, m0))
-
-
-def test_cfg5_full_size_fused_equals_api_chain():
-    q = 2001
-    x = torch.from_numpy(_stack(q, 17, 8)).cuda()
-    dop, grid = kst.make_doppler_grid(q), kst.make_stacked_spatial_grid(P, K, G)
-    vals, summ = process_frame_device(x, K, RB, dop, grid, groups=K)
-    assert tuple(vals.shape) == (K, q, q) and bool(torch.isfinite(vals).all())
-    st = kst.StackedHistory(P, q, K, x)
-    est = kst.multipass_estimate(st, RB)
-    assert est.iterations == int(summ[0]) and est.converged == bool(summ[1])
-    imgs = kst.pass_images(kst.build_filter("kron", estimate=est), st, dop, spatial_count=G)
-    chain = torch.stack([im.values for im in imgs])
-    scale = float(chain.abs().max())
-    assert float((vals - chain).abs().max()) <= 1e-9 * scale

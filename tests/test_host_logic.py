@@ -132,7 +132,12 @@ def test_bench_reference_arm_prints_one_json_line():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["unit"] == "pixels/s" and d["value"] > 0
-    assert d["cpu_baseline"]["kind"] == "port"
+    # the unmodified reference when baseline/_ref is installed, else the port
+    has_ref = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "kronstap"))
+    assert d["cpu_baseline"]["kind"] == ("reference" if has_ref else "port")
+    if has_ref:
+        assert set(d["cpu_baseline"]["modes"]) == {"blas", "pool"}
+        assert d["cpu_baseline"]["host"]["blas"] is not None
     assert d["e2e"]["h2d_bytes_per_step"] == 0
 
 

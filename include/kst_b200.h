@@ -209,6 +209,28 @@ int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins,
                  int drop_temporal, const double* dopplers, int D,
                  const double* grid, int G, double* values, void* stream);
 
+/*
+ * Batched windowed (L-mode) estimator + detector for the test-bin tile
+ * [lo, hi) (same semantics and arguments as kst_windowed over all the tile's
+ * windows; the reference per-window sequence is pkg/README.md:144-161, i.e.
+ * src/lrkron.py:53,118 and src/filters.py:137,243 per window). Every window
+ * is estimated from the banded snapshot Gram (P x P blocks) in one CTA --
+ * no (pq)^2 covariance or q^2 factor per window -- and each test bin is
+ * detected from its window's bin spectra. Windows outside the batched
+ * limits (p > 3, n_w > 128, rank_temporal > 6, G > 64, or a small
+ * eigensolve that does not converge) run on the per-window step path.
+ *   window_info host (optional): 8 ints per window s = window_start(lo) ..
+ *   window_start(hi - 1): {status, iterations, converged, ka, kb,
+ *   Rayleigh-Ritz rounds, r, n_w r}; status 64 = recomputed on the step
+ *   path; all -1 when the whole call took the step path.
+ */
+int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins,
+              int p, int q, int n_w, int64_t lo, int64_t hi, int rank_spatial,
+              int rank_temporal, double tol, int max_iter, int kind,
+              int drop_temporal, const double* dopplers, int D,
+              const double* grid, int G, double* values, int* window_info,
+              void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -48,6 +48,8 @@ _SIGS = {
     "kst_chol": (_i, [_vp, _vp, _i, _vp, _vp]),
     "kst_windowed": (_i, [_vp, _vp, _i64, _i64, _i, _i, _i, _i64, _i64, _i64, _i64, _i64, _i, _i,
                           _d, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp]),
+    "kst_lmode": (_i, [_vp, _vp, _i64, _i64, _i, _i, _i, _i64, _i64, _i, _i, _d, _i, _i, _i, _vp,
+                       _i, _vp, _i, _vp, _vp, _vp]),
     "kst_chol_solve": (_i, [_vp, _vp, _i, _vp, _i64, _vp, _vp]),
     "kst_pipeline": (_i, [_vp, _vp, _i64, _i, _i, _i, _i, _d, _i, _i, _vp, _i, _vp, _i, _i, _vp,
                           _vp, _vp]),

@@ -61,7 +61,7 @@ struct kst_ctx {
     void* ptr = nullptr;
     size_t bytes = 0;
   };
-  Slot slots[24];
+  Slot slots[32];
   // pinned host staging for small device->host reads
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
@@ -127,7 +127,11 @@ enum WsSlot {
   WS_PIPE_SP = 16,  // pipeline: spatial factor + spatial basis
   WS_BZ = 17,       // eigensolver: split-K partials of B*Z
   WS_OZ_SLICES = 18, // int8 Gram: operand slices + column exponents
-  WS_OZ_PROD = 19   // int8 Gram: int32 diagonal products
+  WS_OZ_PROD = 19,  // int8 Gram: int32 diagonal products
+  WS_LM_SPEC = 20,  // L-mode: bin spectra (+ twiddle / grid constants)
+  WS_LM_W = 21,     // L-mode: banded snapshot Gram + row sums
+  WS_LM_E = 22,     // L-mode: per-test-bin projection matrices + window info
+  WS_LM_H = 23      // L-mode: per-CTA eigen scratch (small Grams, residuals)
 };
 
 // Every extern "C" entry point runs on its context's device: the caller's
@@ -293,4 +297,6 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
            const cplx* ub, int kb, int kind, int spatial_only, const double* dop_host, int D,
            const cplx* grid_host, int G, int groups, double* values, cudaStream_t st,
            bool check_finite = true);
+int spectra(kst_ctx* ctx, const cplx* x, int64_t rows, int q, const double* dop_host, int D,
+            cplx* spec, void* consts, cudaStream_t st);
 }  // namespace kst

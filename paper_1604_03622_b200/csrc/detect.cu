@@ -1266,6 +1266,45 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   return KST_OK;
 }
 
+// Unnormalised Doppler spectra of `rows` time rows (length q) at the D
+// Doppler bins: spec[row][d] = sum_t x[t] e^{-2 pi i t f_d} -- the folded
+// Stockham FFT on a uniform grid f_d = d / D, the direct
+// sum with the reference's phase otherwise (src/filters.py:262-264). `consts`
+// is caller-owned device scratch of D complex + D doubles (twiddles, grid).
+// Used by the batched L-mode path (lmode.cu), whose per-bin projections act
+// on these spectra.
+int spectra(kst_ctx* ctx, const cplx* x, int64_t rows, int q, const double* dop_host, int D,
+            cplx* spec, void* consts, cudaStream_t st) {
+  if (rows == 0) return KST_OK;
+  bool uniform = true;
+  for (int d = 0; d < D && uniform; ++d) uniform = dop_host[d] == (double)d / (double)D;
+  Plan plan;
+  if (uniform && (!plan_factors(D, plan) || (size_t)3 * D * sizeof(cplx) > 200 * 1024)) uniform = false;
+  if (!uniform && (size_t)q * sizeof(cplx) > 200 * 1024)
+    return set_err(ctx, KST_ERR_DIMENSION, "spectra: q=%d too long for the direct-sum path", q);
+  cplx* tw = (cplx*)consts;
+  double* dop = (double*)(tw + D);
+  if (uniform) {
+    twiddle_kernel<<<cdiv(D, 256), 256, 0, st>>>(tw, D);
+    KST_LAUNCH(ctx);
+    KST_TRY(const_upload(ctx, (const void*)&c_plan, &plan, sizeof(Plan), st));
+  } else {
+    KST_CUDA(ctx, cudaMemcpyAsync(dop, dop_host, sizeof(double) * D, cudaMemcpyHostToDevice, st));
+    KST_CUDA(ctx, cudaStreamSynchronize(st));  // dop_host is pageable caller memory
+  }
+  const size_t smem = uniform ? sizeof(cplx) * (KST_RS_GTW ? 2 : 3) * D : sizeof(cplx) * q;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    KST_CUDA(ctx, cudaFuncSetAttribute(row_spectrum_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    configured = 226 * 1024;
+  }
+  row_spectrum_kernel<<<(unsigned)rows, NTS, smem, st>>>(x, rows, q, nullptr, 0, tw, D, uniform, dop,
+                                                        spec, nullptr, nullptr);
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}
+
 int filter_cube(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
                 const cplx* ub, int kb, int kind, int spatial_only, cplx* out, cudaStream_t st) {
   if (p < 1 || q < 1 || p > kMaxP || ka < 0 || ka > p || kb < 0 || kb > std::min(q, kMaxKB))

@@ -18,6 +18,7 @@ windows) are detected together in one call.
 
 from __future__ import annotations
 
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 
@@ -43,6 +44,13 @@ def _pool(n):
         if p is None:
             p = _pools[n] = ThreadPoolExecutor(max_workers=n, thread_name_prefix="kst-window")
         return p
+
+
+def last_window_info():
+    """Per-window records of this thread's last batched windowed call: rows
+    {status, iterations, converged, ka, kb, Rayleigh-Ritz rounds, r, n_w r}
+    (include/kst_b200.h kst_lmode); status 64 = recomputed on the step path."""
+    return getattr(_local, "last_window_info", None)
 
 
 def window_start(m, n_w, n_bins):
@@ -97,13 +105,29 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
     starts = list(range(window_start(lo, n_w, n_bins), window_start(hi - 1, n_w, n_bins) + 1))
     ests = {}
     grids = {}
-    # estimates not requested: every window runs inside one C call per worker
-    # (kst_windowed: scm -> lrkron -> bases -> detect per window, no Python
-    # per window); the step-API loop below keeps the per-window estimates
+    # estimates not requested: the whole tile in ONE C call (kst_lmode: the
+    # batched window estimator and detector; it hands windows outside its
+    # limits to the per-window step path itself). The step-API loop below
+    # keeps the per-window estimates (return_estimates) and serves as the
+    # A/B reference path (KST_LMODE=serial).
     fused = not return_estimates and rank_temporal < q and kind in nat.KIND
     if fused:
         grids["dop"], grids["grid"] = _host_grid_args(StapFilter(kind, p, q), dopplers, spatial_grid)
         xc = x.contiguous()
+        if os.environ.get("KST_LMODE", "batched") != "serial":
+            dop, grid = grids["dop"], grids["grid"]
+            c = nat.ctx(x.device)
+            nwin = window_start(hi - 1, n_w, n_bins) - window_start(lo, n_w, n_bins) + 1
+            info = np.zeros((nwin, 8), dtype=np.int32)
+            nat.check(nat.lib().kst_lmode(
+                c, nat.ptr(xc), a, n_bins, p, q, n_w, lo, hi, int(rank_spatial),
+                int(rank_temporal), float(tol), int(max_iter), nat.KIND[kind],
+                int(bool(drop_temporal)), dop.ctypes.data_as(nat.C.c_void_p), dop.size,
+                grid.ctypes.data_as(nat.C.c_void_p), grid.shape[0], nat.ptr(vals),
+                info.ctypes.data_as(nat.C.c_void_p), nat.stream_of(x.device)), c)
+            _local.last_window_info = info
+            dmap = DetectionMap(vals if dev_out else nat.to_host(vals), dop, grid)
+            return dmap
 
     def run_fused(s_begin, s_end, step):
         dop, grid = grids["dop"], grids["grid"]

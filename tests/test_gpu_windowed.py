@@ -110,9 +110,11 @@ def test_concurrent_windows_are_bitwise_serial(workers):
 
 @pytest.mark.parametrize("workers", [1, 4])
 @pytest.mark.parametrize("kind,drop", [("kron", False), ("classical", False), ("kron", True)])
-def test_fused_windows_equal_the_step_api_loop(workers, kind, drop):
-    """kst_windowed (one C call per worker, no per-window Python) gives the
-    step-API loop's map bitwise, also for a tile with halo."""
+def test_fused_windows_equal_the_step_api_loop(workers, kind, drop, monkeypatch):
+    """kst_windowed (one C call per worker, no per-window Python; the serial
+    per-window path the batched kst_lmode falls back to) gives the step-API
+    loop's map bitwise, also for a tile with halo."""
+    monkeypatch.setenv("KST_LMODE", "serial")
     p, q, nb, D, G, n_w = 3, 64, 40, 48, 8, 9
     cube = scenes.bench_scene(p, q, nb, seed=41, movers=3).data[0]
     dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)

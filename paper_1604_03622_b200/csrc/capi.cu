@@ -303,6 +303,18 @@ int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins, in
   std::vector<double> tbv(rank_temporal > 0 ? rank_temporal : 1);
   const cplx* X = (const cplx*)cube;  // bin a of the frame at row 0
   const int h = n_w / 2;
+  // Window Grams run on the FP64 DMMA engine whatever the context's K1
+  // engine: a window's b can have rank n_w r_a < r_b, and the CRT engine's
+  // 2^-32 column rounding lifts its null eigenvalues to ~1e-10 of the top
+  // one -- close enough to the 1e-9 keep threshold (src/filters.py:70) to
+  // admit a spurious basis vector. FP64 keeps them at ~1e-16 (measured at
+  // n_w = 1, r_b = 2).
+  struct EngineGuard {
+    kst_ctx* c;
+    int mode;
+    ~EngineGuard() { c->gram_mode = mode; }
+  } eg{ctx, ctx->gram_mode};
+  ctx->gram_mode = 0;
   for (int64_t s = s_begin; s < s_end; s += s_step) {
     if (s < 0 || s + n_w > n_bins || s < a)
       return set_err(ctx, KST_ERR_DIMENSION, "windowed: window %lld outside the cube",

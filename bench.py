@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="gotcha",
-                    choices=sorted(CONFIGS) + ["lmode", "multipass", "sweep"])
+                    choices=sorted(CONFIGS) + ["lmode", "lmode-gotcha", "multipass", "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # internal: one threading mode of the reference arm (time_reference)
     ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
@@ -382,8 +382,9 @@ def config_block(args, cfg, world):
 # ----------------------------------------------------------------- our arm
 def run_lmode(args, rank, local, world):
     """Supplementary line for configs[3] (L-mode windows): one
-    256 x 256 frame per GPU per step through windowed_detection_image (n_w = 81
-    training bins per test bin, ranks (1, 3)); N > 1 tiles ONE frame's test
+    256 x 256 frame (--config lmode) or one Gotcha-scale 2001 x 2001 frame
+    (--config lmode-gotcha) per GPU per step through windowed_detection_image
+    (n_w = 81 training bins per test bin, ranks (1, 3)); N > 1 tiles ONE frame's test
     bins over the ranks (parallel.tile_bounds), each rank reading its tile plus
     the halo its windows reach, maps all-gathered over NCCL (strong scaling)."""
     import torch
@@ -394,7 +395,9 @@ def run_lmode(args, rank, local, world):
         dist.init_process_group("nccl", device_id=dev)
     import paper_1604_03622_b200 as kst
     from paper_1604_03622_b200 import _native as nat
-    p, q, nb, D, G, ra, rb, n_w = 3, 256, 256, 256, 16, 1, 3, 81
+    gotcha = args.config == "lmode-gotcha"
+    p, q, nb, D, G, ra, rb, n_w = (3, 2001, 2001, 2001, 16, 1, 3, 81) if gotcha else \
+        (3, 256, 256, 256, 16, 1, 3, 81)
     from paper_1604_03622_b200 import parallel
     host = make_frame((p, q, nb, D, G, ra, rb, 1), 17)
     cube = torch.from_numpy(host).to(dev)
@@ -415,6 +418,7 @@ def run_lmode(args, rank, local, world):
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
     launches = nat.lib().kst_launch_count(c) - l0
+    winfo = kst.windowed.last_window_info()
     # end to end: host cube in (this rank's tile + halo), full map gathered
     # over NCCL and copied to the host
     if world > 1:
@@ -435,7 +439,9 @@ def run_lmode(args, rank, local, world):
     base = None
     if not args.no_cpu_baseline:
         from oracle import kron_oracle as orc
-        bins = list(range(0, nb, 32))
+        # bounded sample: a few interior test bins, each its own window
+        # estimate + detection (~9 s per window at Gotcha scale)
+        bins = [nb // 3, nb // 2] if gotcha else list(range(0, nb, 32))
         tc = time.perf_counter()
         orc.windowed(host, n_w, ra, rb, D, G, bins=bins)
         tc = time.perf_counter() - tc
@@ -448,7 +454,8 @@ def run_lmode(args, rank, local, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": DTYPE,
         "data": "synthetic (reference simulator restated in scenes.py; seeded, 8 movers)",
-        "config": {"workload": f"configs[3] L-mode: {nb} bins x {D} Doppler x {G} spatial, p={p} "
+        "config": {"workload": f"configs[3] L-mode{' at Gotcha scale' if gotcha else ''}: "
+                               f"{nb} bins x {D} Doppler x {G} spatial, p={p} "
                                f"q={q}, n_w={n_w} training bins per test bin "
                                f"({nb - n_w + 1} window estimates), ranks ({ra}, {rb})",
                    "parallelism": f"bin tiles + halo x{world}" if world > 1 else "single"},
@@ -456,9 +463,14 @@ def run_lmode(args, rank, local, world):
                 "h2d_bytes_per_step": int(host[a:b].nbytes),
                 "d2h_bytes_per_step": int(nb * D * 8)},
         "gpu_launches": int(launches), "cpu_baseline": base,
+        "window_info": {"fallback_windows": int(np.sum(winfo[:, 0] == 64)) if winfo is not None
+                        else None,
+                        "max_rayleigh_ritz_rounds": int(winfo[:, 5].max()) if winfo is not None
+                        else None},
         "roofline": None,
-        "roofline_note": "latency-bound small per-window kernels (SURVEY.md §8d: no roofline for "
-                         "the eigen stages); the frame headline is configs[1]"}))
+        "roofline_note": "per-window eigensolves are latency chains (SURVEY.md §8d: no roofline "
+                         "for the eigen stages); kernel split in profiles/; the frame headline is "
+                         "configs[1]"}))
 
 
 def run_sweep(args, rank, local, world):
@@ -634,7 +646,7 @@ def main():
     if args.config == "sweep" and args.impl == "ours":
         run_sweep(args, *dist_env())
         return
-    if args.config == "lmode" and args.impl == "ours":
+    if args.config in ("lmode", "lmode-gotcha") and args.impl == "ours":
         run_lmode(args, *dist_env())
         return
     if args.config == "multipass" and args.impl == "ours":

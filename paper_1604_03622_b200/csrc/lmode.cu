@@ -77,13 +77,20 @@ struct BG {
 constexpr int BG_TQ = 16;
 constexpr int BG_LD = BG_TQ + 1;  // padded smem row (bank spread)
 
+// Split-K: blockIdx.y takes pulses [y qs, (y + 1) qs); with nsplit > 1 each
+// split writes its own partial (W + y * wstride, rs + y * rstride) and
+// band_reduce_kernel sums them in split order. nsplit and qs depend on q only
+// (never on the tile), so a tile's W equals the full frame's bitwise.
 template <int P>
 __global__ void __launch_bounds__(NT) band_gram_kernel(const cplx* __restrict__ X, int nb, int q,
-                                                       int n_w, int tb, cplx* __restrict__ W,
-                                                       cplx* __restrict__ rs) {
+                                                       int n_w, int tb, int qs, int64_t wstride,
+                                                       cplx* __restrict__ W, cplx* __restrict__ rs) {
   constexpr int KT = BG<P>::KT;
   extern __shared__ __align__(16) cplx xs[];  // [bin][channel][BG_LD]
   const int m0 = blockIdx.x * tb;
+  const int qa = blockIdx.y * qs, qb = min(q, qa + qs);
+  W += blockIdx.y * wstride;
+  rs += blockIdx.y * (int64_t)nb * P;
   const int nrb = min(tb + n_w - 1, nb - m0);
   const int ngrp = (n_w + KT - 1) / KT;
   const int ml = threadIdx.x / ngrp, og = threadIdx.x % ngrp;
@@ -98,8 +105,8 @@ __global__ void __launch_bounds__(NT) band_gram_kernel(const cplx* __restrict__ 
       for (int j = 0; j < P; ++j) acc[k][i][j] = cmk(0, 0);
 #pragma unroll
   for (int i = 0; i < P; ++i) racc[i] = cmk(0, 0);
-  for (int t0 = 0; t0 < q; t0 += BG_TQ) {
-    const int tl = min(BG_TQ, q - t0);
+  for (int t0 = qa; t0 < qb; t0 += BG_TQ) {
+    const int tl = min(BG_TQ, qb - t0);
     __syncthreads();  // previous chunk consumed
     for (int e = threadIdx.x; e < nrb * P * BG_TQ; e += NT) {
       const int r = e / BG_TQ, c = e - r * BG_TQ;
@@ -151,6 +158,25 @@ __global__ void __launch_bounds__(NT) band_gram_kernel(const cplx* __restrict__ 
   if (og == 0)
 #pragma unroll
     for (int i = 0; i < P; ++i) rs[(int64_t)m * P + i] = racc[i];
+}
+
+// W = sum over splits in split order (and the row sums)
+__global__ void band_reduce_kernel(const cplx* __restrict__ Wp, int nsplit, int64_t wcount,
+                                   int64_t wstride, int64_t rcount, cplx* __restrict__ W,
+                                   cplx* __restrict__ rs) {
+  const cplx* rsp = Wp + nsplit * wstride;  // partial row sums follow the W partials
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < wcount + rcount;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    cplx acc = cmk(0, 0);
+    if (e < wcount) {
+      for (int k = 0; k < nsplit; ++k) acc = cadd(acc, Wp[k * wstride + e]);
+      W[e] = acc;
+    } else {
+      const int64_t r = e - wcount;
+      for (int k = 0; k < nsplit; ++k) acc = cadd(acc, rsp[k * rcount + r]);
+      rs[r] = acc;
+    }
+  }
 }
 
 // W_{mA,mB}[i][j] from the band (mA, mB bin indices of the tile cube)
@@ -233,50 +259,61 @@ __device__ __forceinline__ void block_gram(const cplx* A, const cplx* B, int nb,
   __syncthreads();
 }
 
-// Cholesky-QR of the nb x s block Y (in place): G = Y^H Y = R^H R, Y <- Y R^-1.
-// Returns false on a non-positive pivot (rank-deficient block).
-__device__ bool chol_qr(cplx* Y, int nb, int s, cplx* G, int* flag) {
-  block_gram(Y, Y, nb, s, G);
-  if (threadIdx.x == 0) {
-    // in-place upper Cholesky factor R of G (row-major, G = R^H R)
-    int ok = 1;
-    for (int k = 0; k < s && ok; ++k) {
-      double d = G[k * LM_S + k].x;
-      for (int i = 0; i < k; ++i) d -= cabs2(G[i * LM_S + k]);
-      if (!(d > 0.0)) {
-        ok = 0;
-        break;
+// Orthonormalise the nb x s block Y in place by classical Gram-Schmidt with
+// reorthogonalisation (CGS2), column by column: stable for the very
+// ill-conditioned blocks a dominant mover produces after one H step (where
+// Cholesky-QR, which squares the condition number, breaks down). A column
+// that vanishes after projection (relative 1e-13) is replaced by the next
+// unused unit vector and re-projected. Warp j forms coefficient j (lanes
+// stride the rows, fixed shuffle tree: deterministic).
+__device__ void cgs2(cplx* Y, int nb, int s, cplx* coef, double* nrm, int* next_unit) {
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = 0; k < s; ++k) {
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      // |y_k|^2 before projection
+      if (wid == 0) {
+        double a = 0.0;
+        for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
+        a = warp_sum(a);
+        if (lane == 0) nrm[0] = a;
       }
-      d = sqrt(d);
-      G[k * LM_S + k] = cmk(d, 0.0);
-      for (int j = k + 1; j < s; ++j) {
-        cplx x = G[k * LM_S + j];
-        for (int i = 0; i < k; ++i) x = csub(x, cmul(cconj(G[i * LM_S + k]), G[i * LM_S + j]));
-        G[k * LM_S + j] = cscale(x, 1.0 / d);
+      for (int pass = 0; pass < 2 && k > 0; ++pass) {
+        __syncthreads();
+        if (wid < k) {
+          cplx acc = cmk(0, 0);
+          for (int r = lane; r < nb; r += 32) cfmca(acc, Y[r * LM_S + wid], Y[r * LM_S + k]);
+          acc.x = warp_sum(acc.x);
+          acc.y = warp_sum(acc.y);
+          if (lane == 0) coef[wid] = acc;
+        }
+        __syncthreads();
+        for (int r = threadIdx.x; r < nb; r += NT) {
+          cplx y = Y[r * LM_S + k];
+          for (int j2 = 0; j2 < k; ++j2) y = csub(y, cmul(Y[r * LM_S + j2], coef[j2]));
+          Y[r * LM_S + k] = y;
+        }
       }
+      __syncthreads();
+      if (wid == 0) {
+        double a = 0.0;
+        for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
+        a = warp_sum(a);
+        if (lane == 0) nrm[1] = a;
+      }
+      __syncthreads();
+      const bool ok = nrm[1] > 1e-26 * nrm[0] && nrm[1] > 0.0;
+      if (ok || attempt == 1) break;
+      // dependent column: restart it as the next unit vector
+      __syncthreads();
+      const int u = *next_unit % nb;
+      for (int r = threadIdx.x; r < nb; r += NT) Y[r * LM_S + k] = cmk(r == u ? 1.0 : 0.0, 0.0);
+      __syncthreads();
+      if (threadIdx.x == 0) *next_unit = u + 1;
     }
-    *flag = ok;
+    const double inv = nrm[1] > 0.0 ? 1.0 / sqrt(nrm[1]) : 0.0;
+    for (int r = threadIdx.x; r < nb; r += NT) Y[r * LM_S + k] = cscale(Y[r * LM_S + k], inv);
+    __syncthreads();
   }
-  __syncthreads();
-  if (!*flag) return false;
-  // Y <- Y R^-1 row by row (forward substitution y R = x)
-  for (int r = threadIdx.x; r < nb; r += NT) {
-    cplx y[LM_S];
-#pragma unroll
-    for (int k = 0; k < LM_S; ++k) {
-      if (k >= s) break;
-      cplx x = Y[r * LM_S + k];
-#pragma unroll
-      for (int i = 0; i < LM_S; ++i)
-        if (i < k) x = csub(x, cmul(y[i], G[i * LM_S + k]));
-      y[k] = cscale(x, 1.0 / G[k * LM_S + k].x);
-    }
-#pragma unroll
-    for (int k = 0; k < LM_S; ++k)
-      if (k < s) Y[r * LM_S + k] = y[k];
-  }
-  __syncthreads();
-  return true;
 }
 
 // Y <- Y Q (nb x s times s x s, Q taken as column `order[k]` of the Jacobi V)
@@ -324,6 +361,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
   cplx* Y = (cplx*)(scratch + 256);
   cplx* Z = Y + (size_t)g.nbmax * LM_S;
   cplx* gam = Z + (size_t)g.nbmax * LM_S;  // n_w P x LM_KBMAX
+  cplx* cmall = gam + (size_t)g.n_w * P * LM_KBMAX;  // (n_w / 2 + 1) x P x LM_KBMAX
   __shared__ double red[4 + 2 * U + 2 * E];
   __shared__ double recv[NREC];
   __shared__ IterState st;
@@ -332,9 +370,11 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
   __shared__ cplx ua[P * P], av[P * P], Q1[P * P], Q2[P * P];
   __shared__ double lamv[P], omega[P], theta[LM_S];
   __shared__ cplx G8[LM_S * LM_S];
-  __shared__ cplx cm[P * LM_KBMAX];
   __shared__ int ka_s, r_s, kb_s, flag_s, status_s, rounds_s, mode_s, spat_s, kk_s;
   __shared__ int sel[LM_S];
+  __shared__ double nrm2[2];
+  __shared__ cplx coefs[LM_S];
+  __shared__ int unit_s;
   const int tid = threadIdx.x;
   const int n_w = g.n_w;
   const double nn = (double)n_w;
@@ -501,6 +541,9 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
         inf[0] = LM_FALLBACK;
         inf[1] = iters;
         inf[2] = conv;
+        inf[3] = 1;  // reason: n_w r outside the batched limit
+        inf[6] = r;
+        inf[7] = nb;
       }
       continue;
     }
@@ -556,17 +599,18 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
           const int row = e / LM_S, k = e % LM_S;
           Y[e] = cmk((k < sb && sel[k] == row) ? 1.0 : 0.0, 0.0);
         }
+        if (tid == 0) unit_s = 0;
         __syncthreads();
         bool done = false;
         int round = 0;
         double prev_worst = 1e300;
         int stall = 0;
         for (; round < LM_MAXR && !done; ++round) {
-          // two power steps (H^2), orthonormalise (Cholesky-QR twice)
+          // two power steps, each followed by CGS2 orthonormalisation
           hmul(H, nb, Y, Z, sb);
+          cgs2(Z, nb, sb, coefs, nrm2, &unit_s);
           hmul(H, nb, Z, Y, sb);
-          if (!chol_qr(Y, nb, sb, G8, &flag_s) || !chol_qr(Y, nb, sb, G8, &flag_s))
-            break;
+          cgs2(Y, nb, sb, coefs, nrm2, &unit_s);
           if (round < 1) continue;  // H^4 warm-up before the first Rayleigh-Ritz
           hmul(H, nb, Y, Z, sb);
           block_gram(Y, Z, nb, sb, G8);  // T = Y^H H Y
@@ -609,15 +653,20 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
           __syncthreads();
           done = flag_s != 0;
         }
-        if (tid == 0) rounds_s = round;
+        __syncthreads();
         if (!done) {
           if (tid == 0) {
             inf[0] = LM_FALLBACK;
             inf[1] = iters;
             inf[2] = conv;
+            inf[3] = rounds_s < 0 ? 2 : 3;  // reason: Cholesky-QR breakdown / no convergence
+            inf[5] = rounds_s < 0 ? -rounds_s - 1 : round;
+            inf[6] = r;
+            inf[7] = nb;
           }
           continue;
         }
+        if (tid == 0) rounds_s = round;
       }
       // ------------------------------------------------------ (6) kept temporal rank
       if (tid == 0) {
@@ -683,46 +732,50 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
     t0 = max(t0, g.lo);
     t1 = min(t1, g.hi);
     const int nwp = n_w * P;
-    for (int64_t t = t0; t < t1; ++t) {
-      const int ml = (int)(t - s_abs);
-      if (kb > 0) {
-        // C[i, j] = sum_{m'k'} conj(alpha[(m'k'), j]) (W_{ml m'} a_k')[i]
-        const int wid = tid >> 5, lane = tid & 31;
-        for (int o = wid; o < P * kb; o += NT / 32) {
-          const int i = o / kb, jj = o - i * kb;
-          const double it = 1.0 / sqrt(theta[jj]);
-          cplx acc = cmk(0, 0);
-          for (int c = lane; c < nb; c += 32) {
-            const int m2 = c / r, k2 = c - m2 * r;
-            cplx wa = cmk(0, 0);
+    const int ntw = (int)(t1 - t0);  // test bins of this window (<= n_w / 2 + 1)
+    if (kb > 0 && ntw > 0) {
+      // C_t[i, j] = sum_{m'k'} conj(alpha[(m'k'), j]) (W_{ml m'} a_k')[i], all test bins:
+      // warp per (bin, i, j) output, lanes stride the n_w r window columns
+      const int wid = tid >> 5, lane = tid & 31;
+      for (int o = wid; o < ntw * P * kb; o += NT / 32) {
+        const int tb = o / (P * kb), rem = o - tb * P * kb, i = rem / kb, jj = rem - i * kb;
+        const int ml = (int)(t0 + tb - s_abs);
+        const double it = 1.0 / sqrt(theta[jj]);
+        cplx acc = cmk(0, 0);
+        for (int c = lane; c < nb; c += 32) {
+          const int m2 = c / r, k2 = c - m2 * r;
+          cplx wa = cmk(0, 0);
 #pragma unroll
-            for (int l = 0; l < P; ++l) cfma(wa, wget<P>(W, n_w, s + ml, s + m2, i, l), av[l * P + k2]);
-            const cplx alc = cscale(Y[c * LM_S + jj], sqrt(omega[k2]) * it);  // conj(alpha)
-            cfma(acc, alc, wa);
-          }
-          acc.x = warp_sum(acc.x);
-          acc.y = warp_sum(acc.y);
-          if (lane == 0) cm[i * LM_KBMAX + jj] = acc;
+          for (int l = 0; l < P; ++l) cfma(wa, wget<P>(W, n_w, s + ml, s + m2, i, l), av[l * P + k2]);
+          const cplx alc = cscale(Y[c * LM_S + jj], sqrt(omega[k2]) * it);  // conj(alpha)
+          cfma(acc, alc, wa);
         }
-        __syncthreads();
-      }
-      cplx* Er = Eout + (size_t)(t - g.lo) * P * nwp;
-      for (int e = tid; e < P * nwp; e += NT) {
-        const int i = e / nwp, col = e - i * nwp, m2 = col / P, l = col - m2 * P;
-        cplx x = m2 == ml ? Q1[i * P + l] : cmk(0, 0);
-        if (kb > 0) {
-          cplx dl = cmk(0, 0);
-          for (int i2 = 0; i2 < P; ++i2) {
-            cplx cg = cmk(0, 0);
-            for (int jj = 0; jj < kb; ++jj) cfma(cg, cm[i2 * LM_KBMAX + jj], gam[col * LM_KBMAX + jj]);
-            cfma(dl, Q2[i * P + i2], cg);
-          }
-          x = csub(x, dl);
-        }
-        Er[e] = x;
+        acc.x = warp_sum(acc.x);
+        acc.y = warp_sum(acc.y);
+        if (lane == 0) cmall[(tb * P + i) * LM_KBMAX + jj] = acc;
       }
       __syncthreads();
     }
+    // E_t[i, (m', l)] = Q1[i, l] [m' = ml] - sum_i2 Q2[i, i2] sum_j C_t[i2, j] gamma[(m' l), j]
+    for (int64_t e = tid; e < (int64_t)ntw * P * nwp; e += NT) {
+      const int tb = (int)(e / (P * nwp));
+      const int rem = (int)(e - (int64_t)tb * P * nwp), i = rem / nwp, col = rem - i * nwp;
+      const int m2 = col / P, l = col - m2 * P;
+      const int ml = (int)(t0 + tb - s_abs);
+      cplx x = m2 == ml ? Q1[i * P + l] : cmk(0, 0);
+      if (kb > 0) {
+        cplx dl = cmk(0, 0);
+        for (int i2 = 0; i2 < P; ++i2) {
+          cplx cg = cmk(0, 0);
+          for (int jj = 0; jj < kb; ++jj)
+            cfma(cg, cmall[(tb * P + i2) * LM_KBMAX + jj], gam[col * LM_KBMAX + jj]);
+          cfma(dl, Q2[i * P + i2], cg);
+        }
+        x = csub(x, dl);
+      }
+      Eout[(size_t)(t0 + tb - g.lo) * P * nwp + rem] = x;
+    }
+    __syncthreads();
     if (tid == 0) {
       inf[0] = 0;
       inf[1] = zero_s ? 0 : iters;
@@ -820,21 +873,38 @@ __global__ void __launch_bounds__(NT) lm_detect_kernel(const cplx* __restrict__ 
   }
 }
 
-size_t window_smem(int nbmax, int nwp) {
+size_t window_smem(int nbmax, int n_w, int p) {
   const size_t jbytes = (kstj::jac_smem_bytes(LM_JAC) + 15) / 16 * 16;
-  return jbytes + sizeof(double) * 256 + sizeof(cplx) * (2 * (size_t)nbmax * LM_S + (size_t)nwp * LM_KBMAX);
+  return jbytes + sizeof(double) * 256 +
+         sizeof(cplx) * (2 * (size_t)nbmax * LM_S + (size_t)n_w * p * LM_KBMAX +
+                         (size_t)(n_w / 2 + 1) * p * LM_KBMAX);
 }
+
+int band_splits(int q) { return std::max(1, std::min(8, q / 32)); }
 
 template <int P>
 int launch_band(kst_ctx* ctx, const cplx* X, int nb, int q, int n_w, cplx* W, cplx* rs,
-                cudaStream_t st) {
+                cplx* Wp, cudaStream_t st) {
   constexpr int KT = BG<P>::KT;
   const int ngrp = (n_w + KT - 1) / KT;
   const int tb = std::max(1, NT / ngrp);
   const size_t smem = sizeof(cplx) * (size_t)(tb + n_w - 1) * P * BG_LD;
+  const int nsplit = band_splits(q);
+  const int qs = ((q + nsplit - 1) / nsplit + BG_TQ - 1) / BG_TQ * BG_TQ;
+  const int64_t wcount = (int64_t)nb * n_w * P * P, rcount = (int64_t)nb * P;
   KST_CUDA(ctx, cudaFuncSetAttribute(band_gram_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-  band_gram_kernel<P><<<cdiv(nb, tb), NT, smem, st>>>(X, nb, q, n_w, tb, W, rs);
+  if (nsplit == 1) {
+    band_gram_kernel<P><<<dim3(cdiv(nb, tb), 1), NT, smem, st>>>(X, nb, q, n_w, tb, qs, 0, W, rs);
+    KST_LAUNCH(ctx);
+    return KST_OK;
+  }
+  const int ny = (q + qs - 1) / qs;
+  band_gram_kernel<P><<<dim3(cdiv(nb, tb), ny), NT, smem, st>>>(X, nb, q, n_w, tb, qs, wcount, Wp,
+                                                                Wp + ny * wcount);
+  KST_LAUNCH(ctx);
+  band_reduce_kernel<<<(unsigned)std::min<int64_t>(cdiv(wcount + rcount, 256), 4096), 256, 0, st>>>(
+      Wp, ny, wcount, wcount, rcount, W, rs);
   KST_LAUNCH(ctx);
   return KST_OK;
 }
@@ -915,7 +985,10 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   // workspace
   char* wspec = (char*)ws_get(ctx, WS_LM_SPEC, sizeof(cplx) * ((size_t)nb * p * D + D + (size_t)G * p) +
                                                    sizeof(double) * D + 256);
-  char* wW = (char*)ws_get(ctx, WS_LM_W, sizeof(cplx) * ((size_t)nb * n_w * p * p + (size_t)nb * p) + 256);
+  const int nsplit = band_splits(q);
+  // W + row sums, then (split-K) nsplit partial copies of both
+  char* wW = (char*)ws_get(ctx, WS_LM_W, sizeof(cplx) * ((size_t)nb * n_w * p * p + (size_t)nb * p) *
+                                             (nsplit > 1 ? nsplit + 1 : 1) + 256);
   char* wE = (char*)ws_get(ctx, WS_LM_E, sizeof(cplx) * (size_t)n_test * p * nwp +
                                              sizeof(int) * (size_t)nwin * WI + sizeof(double) * nwin + 256);
   char* wH = (char*)ws_get(ctx, WS_LM_H, sizeof(cplx) * (size_t)nslot * nbmax * nbmax +
@@ -927,6 +1000,7 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   void* consts = hconj + (size_t)G * p;
   cplx* W = (cplx*)wW;
   cplx* rs = W + (size_t)nb * n_w * p * p;
+  cplx* Wp = rs + (size_t)nb * p;  // split-K partials (nsplit > 1)
   cplx* E = (cplx*)wE;
   int* dinfo = (int*)(E + (size_t)n_test * p * nwp);
   double* dres = (double*)(((uintptr_t)(dinfo + (size_t)nwin * WI) + 15) & ~(uintptr_t)15);
@@ -942,9 +1016,9 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   KST_TRY(kst::spectra(ctx, X, (int64_t)nb * p, q, dopplers, D, spec, consts, st));
   // 2. banded snapshot Gram + row sums
   switch (p) {
-    case 1: KST_TRY(launch_band<1>(ctx, X, nb, q, n_w, W, rs, st)); break;
-    case 2: KST_TRY(launch_band<2>(ctx, X, nb, q, n_w, W, rs, st)); break;
-    default: KST_TRY(launch_band<3>(ctx, X, nb, q, n_w, W, rs, st)); break;
+    case 1: KST_TRY(launch_band<1>(ctx, X, nb, q, n_w, W, rs, Wp, st)); break;
+    case 2: KST_TRY(launch_band<2>(ctx, X, nb, q, n_w, W, rs, Wp, st)); break;
+    default: KST_TRY(launch_band<3>(ctx, X, nb, q, n_w, W, rs, Wp, st)); break;
   }
   KST_LAUNCH(ctx);
   // 3. one CTA per window (persistent over nslot CTAs)
@@ -965,7 +1039,7 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   wa.nslot = nslot;
   wa.nbmax = nbmax;
   wa.tol = tol;
-  const size_t wsm = window_smem(nbmax, nwp);
+  const size_t wsm = window_smem(nbmax, n_w, p);
   switch (p) {
     case 1: KST_TRY(launch_win<1>(ctx, W, rs, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
     case 2: KST_TRY(launch_win<2>(ctx, W, rs, wa, H, rscr, E, dinfo, dres, wsm, st)); break;

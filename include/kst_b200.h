@@ -75,6 +75,14 @@ long long kst_launch_count(const kst_ctx* ctx);
  * context creation. */
 int kst_set_gram(kst_ctx* ctx, int mode, int slices);
 int kst_get_gram(const kst_ctx* ctx, int* mode, int* slices);
+/* Detection (K5) precision. bits = 32 (default): FP64 load pass (spatial
+ * reduction, temporal-projection coefficients) + FP32 prime-factor DFT and
+ * pixel stage (detect_f32.cu) for single-map uniform-grid detection with
+ * p <= 4, kb <= 3, q <= D and D a product of coprime factors <= 32 (or a*b,
+ * a, b <= 32); every other case runs the FP64 kernels. bits = 64: the FP64
+ * kernels everywhere. Env KST_DETECT=f32|f64 sets it at context creation. */
+int kst_set_detect(kst_ctx* ctx, int bits);
+int kst_get_detect(const kst_ctx* ctx, int* bits);
 /* int8 tensor ops issued by the last int8 Gram (0 if none); with profiling on,
  * kst_stage_times entry 5 is that Gram's int8 GEMM span in ms. */
 double kst_gram_int8_ops(const kst_ctx* ctx);

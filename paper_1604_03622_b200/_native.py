@@ -33,6 +33,8 @@ _SIGS = {
     "kst_set_gram": (_i, [_vp, _i, _i]),
     "kst_get_gram": (_i, [_vp, _ip, _ip]),
     "kst_gram_int8_ops": (_d, [_vp]),
+    "kst_set_detect": (_i, [_vp, _i]),
+    "kst_get_detect": (_i, [_vp, _ip]),
     "kst_set_profiling": (_i, [_vp, _i]),
     "kst_stage_times": (_i, [_vp, _vp, _i]),
     "kst_scm": (_i, [_vp, _vp, _i64, _i64, _vp, _vp]),

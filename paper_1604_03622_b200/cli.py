@@ -176,8 +176,12 @@ def cmd_filter(args):
 
 def cmd_detect(args):
     """`src/cli.py:209-240`: detection map, or the two-pass change map."""
-    from .filters import detection_image, make_doppler_grid, make_spatial_grid
+    from .filters import detection_image, make_doppler_grid, make_spatial_grid, set_detect_precision
     from .multipass import change_detect, pass_images, stack_passes
+    # the CLI writes the reference's map files: FP64 detection, so the CSV
+    # matches what the reference CLI writes to ~1e-12 (the library default,
+    # FP32 detection, holds the SURVEY.md §8c comparator)
+    set_detect_precision("f64")
     hist, _ = formats.load_cube(args.input)
     est = formats.read_estimate(args.estimate)
     dopplers = make_doppler_grid(args.grid_doppler)

@@ -109,6 +109,8 @@ int kst_ctx_create(int device, kst_ctx** out) {
   if (const char* e = getenv("KST_GRAM_SLICES"))
     c->gram_slices = c->gram_mode >= 2 ? std::min(14, std::max(8, atoi(e)))
                                        : std::min(8, std::max(3, atoi(e)));
+  // K5 precision default: FP32 transform; KST_DETECT=f64 overrides
+  if (const char* e = getenv("KST_DETECT")) c->det_bits = strcmp(e, "f64") == 0 ? 64 : 32;
   DeviceGuard g(device);
   cudaFree(nullptr);  // establish the primary context
   *out = c;
@@ -147,6 +149,19 @@ int kst_set_gram(kst_ctx* ctx, int mode, int slices) {
     return set_err(ctx, KST_ERR_CUDA, "int8 Gram unavailable: cuBLAS not loadable");
   ctx->gram_mode = mode;
   if (mode != 0) ctx->gram_slices = slices;
+  return KST_OK;
+}
+
+int kst_set_detect(kst_ctx* ctx, int bits) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  if (bits != 32 && bits != 64) return set_err(ctx, KST_ERR_DIMENSION, "detection precision must be 32 or 64");
+  ctx->det_bits = bits;
+  return KST_OK;
+}
+
+int kst_get_detect(const kst_ctx* ctx, int* bits) {
+  if (!ctx) return KST_ERR_DIMENSION;
+  if (bits) *bits = ctx->det_bits;
   return KST_OK;
 }
 
@@ -249,7 +264,8 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   stage_mark(ctx, 1, st);
   // the temporal basis must survive until detection: dedicated slot
   const bool full_b = rank_temporal == q;
-  cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal + 64);
+  // ub: the top-rb eigenvectors (q x rb), then the kept kb columns repacked (q x kb)
+  cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);
   cplx* temporal = full_b ? (cplx*)ws_get(ctx, WS_PIPE_T, sizeof(cplx) * (size_t)q * q) : nullptr;
   if (!ub || (full_b && !temporal)) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
   std::vector<double> tbv(rank_temporal > 0 ? rank_temporal : 1);
@@ -266,8 +282,16 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   } else if (tbv[0] > 0.0) {
     while (kb < rank_temporal && tbv[kb] > 1e-9 * tbv[0]) ++kb;
   }
+  // kb < rb (b of rank below r_b): detect takes a q x kb basis
+  const cplx* ubk = ub;
+  if (!full_b && kb > 0 && kb < rank_temporal) {
+    cplx* packed = ub + (size_t)q * rank_temporal;
+    KST_CUDA(ctx, cudaMemcpy2DAsync(packed, sizeof(cplx) * kb, ub, sizeof(cplx) * rank_temporal,
+                                    sizeof(cplx) * kb, q, cudaMemcpyDeviceToDevice, st));
+    ubk = packed;
+  }
   stage_mark(ctx, 3, st);
-  KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, ka ? ua : nullptr, ka, kb ? ub : nullptr, kb,
+  KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, ka ? ua : nullptr, ka, kb ? ubk : nullptr, kb,
                       kind, 0, dopplers, D, (const cplx*)grid, G, groups, values, st,
                       /*check_finite=*/false));  // a non-finite cube already failed lrkron
   stage_mark(ctx, 4, st);
@@ -297,7 +321,8 @@ int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins, in
     return set_err(ctx, KST_ERR_DIMENSION, "windowed: rank_temporal == q needs the step API");
   cplx* S = (cplx*)ws_get(ctx, WS_S, sizeof(cplx) * d * d);
   cplx* spatial = (cplx*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 2 + 64);
-  cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal + 64);
+  // ub: the top-rb eigenvectors (q x rb), then the kept kb columns repacked (q x kb)
+  cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);
   if (!S || !spatial || !ub) return set_err(ctx, KST_ERR_CUDA, "windowed: workspace");
   cplx* ua = spatial + p * p;
   std::vector<double> tbv(rank_temporal > 0 ? rank_temporal : 1);
@@ -315,6 +340,14 @@ int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins, in
     ~EngineGuard() { c->gram_mode = mode; }
   } eg{ctx, ctx->gram_mode};
   ctx->gram_mode = 0;
+  // and the per-window detection runs in FP64 like the batched L-mode
+  // detector (lmode.cu lm_detect_kernel), whatever the context's K5 precision
+  struct DetGuard {
+    kst_ctx* c;
+    int bits;
+    ~DetGuard() { c->det_bits = bits; }
+  } dg{ctx, ctx->det_bits};
+  ctx->det_bits = 64;
   for (int64_t s = s_begin; s < s_end; s += s_step) {
     if (s < 0 || s + n_w > n_bins || s < a)
       return set_err(ctx, KST_ERR_DIMENSION, "windowed: window %lld outside the cube",
@@ -329,13 +362,21 @@ int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins, in
     KST_TRY(kst::subspace_basis(ctx, spatial, p, rank_spatial, 1e-9, ua, &ka, st));
     if (tbv[0] > 0.0)
       while (kb < rank_temporal && tbv[kb] > 1e-9 * tbv[0]) ++kb;
+    // kb < rb (a window's b of rank n_w r_a < r_b): detect takes a q x kb basis
+    const cplx* ubk = ub;
+    if (kb > 0 && kb < rank_temporal) {
+      cplx* packed = ub + (size_t)q * rank_temporal;
+      KST_CUDA(ctx, cudaMemcpy2DAsync(packed, sizeof(cplx) * kb, ub, sizeof(cplx) * rank_temporal,
+                                      sizeof(cplx) * kb, q, cudaMemcpyDeviceToDevice, st));
+      ubk = packed;
+    }
     // test bins sharing window s (windowed.window_bins), clipped to the tile
     int64_t t0 = (s == 0) ? 0 : s + h, t1 = (s == n_bins - n_w) ? n_bins : s + h + 1;
     t0 = std::max(t0, lo);
     t1 = std::min(t1, hi);
     if (t1 <= t0) continue;
     KST_TRY(kst::detect(ctx, X + (t0 - a) * d, t1 - t0, p, q, ka ? ua : nullptr, ka,
-                        kb ? ub : nullptr, kb, kind, drop_temporal, dopplers, D,
+                        kb ? ubk : nullptr, kb, kind, drop_temporal, dopplers, D,
                         (const cplx*)grid, G, 1, values + (t0 - lo) * D, st, false));
   }
   return KST_OK;

@@ -80,6 +80,11 @@ struct kst_ctx {
   // Dopplers, twiddles): the key they were uploaded for
   const void* det_base = nullptr;
   std::vector<double> det_key;
+  // K5 precision: 32 = FP32 prime-factor transform (detect_f32.cu) where it
+  // applies, 64 = the FP64 kernels; position maps resident for f32_D
+  int det_bits = 32;
+  const void* f32_base = nullptr;
+  int f32_D = 0;
   long long launches = 0;
   int profiling = 0;
   // NVTX ranges of the kst_pipeline stages (kst.scm, kst.lrkron, kst.bases,
@@ -131,7 +136,8 @@ enum WsSlot {
   WS_LM_SPEC = 20,  // L-mode: bin spectra (+ twiddle / grid constants)
   WS_LM_W = 21,     // L-mode: banded snapshot Gram + row sums
   WS_LM_E = 22,     // L-mode: per-test-bin projection matrices + window info
-  WS_LM_H = 23      // L-mode: per-CTA eigen scratch (small Grams, residuals)
+  WS_LM_H = 23,     // L-mode: per-CTA eigen scratch (small Grams, residuals)
+  WS_DET32 = 24     // FP32 detection: prime-factor position maps
 };
 
 // Every extern "C" entry point runs on its context's device: the caller's
@@ -299,4 +305,10 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
            bool check_finite = true);
 int spectra(kst_ctx* ctx, const cplx* x, int64_t rows, int q, const double* dop_host, int D,
             cplx* spec, void* consts, cudaStream_t st);
+// detect_f32.cu: FP32 single-map detection (uniform grid); -1 = not taken
+bool detect_f32_supported(int p, int q, int ka, int kb, int mode, int spatial, int D, int G);
+int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
+               const cplx* ub, int kb, int mode, int spatial, int D, const cplx* ubspec,
+               const cplx* hconj, const cplx* grid_host, int G, bool dft, double* values,
+               int* flag, cudaStream_t st);
 }  // namespace kst

@@ -1137,8 +1137,11 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   // fused per-bin kernel (no spectra in HBM) when the plan fits it
   FusedArgs fa;
   static const bool fused_on = !(getenv("KST_DET_FUSED") && atoi(getenv("KST_DET_FUSED")) == 0);
-  const bool fused = uniform && fused_on && fused_ok(plan, p, q, D, kb_used, G);
-  const int64_t srows = fused ? 0 : rows;  // spectra / coefficient rows in HBM
+  // FP32 prime-factor kernel (detect_f32.cu) at det_bits = 32, else the FP64 kernels
+  const bool f32 = uniform && ctx->det_bits == 32 && groups == 1 &&
+                   detect_f32_supported(p, q, has_a ? ka : 0, kb_used, mode, spatial, D, G);
+  const bool fused = !f32 && uniform && fused_on && fused_ok(plan, p, q, D, kb_used, G);
+  const int64_t srows = (fused || f32) ? 0 : rows;  // spectra / coefficient rows in HBM
   // workspace: spec (srows x D), coef (srows x kb), ubspec (kb x D), ubT (kb x q),
   // twiddles (D), hconj (G x p), dop (D), flag (2), perm (D)
   const size_t bytes = sizeof(cplx) * ((size_t)srows * D + (size_t)srows * std::max(kb_used, 1) +
@@ -1198,7 +1201,13 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
                                                    ubspec, nullptr, flag + 1);
     KST_LAUNCH(ctx);
   }
-  if (fused) {
+  if (f32) {
+    const bool dft = G % 4 == 0 && dft_grid(grid_host, G, p);
+    const int rc = detect_f32(ctx, cube, n, p, q, has_a ? ua : nullptr, has_a ? ka : 0, ub, kb_used,
+                              mode, spatial, D, ubspec, hconj, grid_host, G, dft, values,
+                              check_finite ? flag : nullptr, st);
+    if (rc != KST_OK) return rc == -1 ? set_err(ctx, KST_ERR_CUDA, "detect_f32: plan rejected") : rc;
+  } else if (fused) {
     fa.P = p;
     fa.q = q;
     fa.D = D;

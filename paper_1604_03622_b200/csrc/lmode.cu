@@ -732,50 +732,57 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
     t0 = max(t0, g.lo);
     t1 = min(t1, g.hi);
     const int nwp = n_w * P;
-    const int ntw = (int)(t1 - t0);  // test bins of this window (<= n_w / 2 + 1)
-    if (kb > 0 && ntw > 0) {
-      // C_t[i, j] = sum_{m'k'} conj(alpha[(m'k'), j]) (W_{ml m'} a_k')[i], all test bins:
-      // warp per (bin, i, j) output, lanes stride the n_w r window columns
-      const int wid = tid >> 5, lane = tid & 31;
-      for (int o = wid; o < ntw * P * kb; o += NT / 32) {
-        const int tb = o / (P * kb), rem = o - tb * P * kb, i = rem / kb, jj = rem - i * kb;
-        const int ml = (int)(t0 + tb - s_abs);
-        const double it = 1.0 / sqrt(theta[jj]);
-        cplx acc = cmk(0, 0);
-        for (int c = lane; c < nb; c += 32) {
-          const int m2 = c / r, k2 = c - m2 * r;
-          cplx wa = cmk(0, 0);
+    // test bins of this window: <= n_w / 2 + 1, except a lone window
+    // (n_w = n_bins) that owns every bin -- C_t is staged CH bins at a time
+    const int CH = n_w / 2 + 1;
+    for (int64_t c0 = t0; c0 < t1; c0 += CH) {
+      const int64_t c1 = min(t1, c0 + CH);
+      const int ntw = (int)(c1 - c0);
+      if (kb > 0 && ntw > 0) {
+        // C_t[i, j] = sum_{m'k'} conj(alpha[(m'k'), j]) (W_{ml m'} a_k')[i], all test bins:
+        // warp per (bin, i, j) output, lanes stride the n_w r window columns
+        const int wid = tid >> 5, lane = tid & 31;
+        for (int o = wid; o < ntw * P * kb; o += NT / 32) {
+          const int tb = o / (P * kb), rem = o - tb * P * kb, i = rem / kb, jj = rem - i * kb;
+          const int ml = (int)(c0 + tb - s_abs);
+          const double it = 1.0 / sqrt(theta[jj]);
+          cplx acc = cmk(0, 0);
+          for (int c = lane; c < nb; c += 32) {
+            const int m2 = c / r, k2 = c - m2 * r;
+            cplx wa = cmk(0, 0);
 #pragma unroll
-          for (int l = 0; l < P; ++l) cfma(wa, wget<P>(W, n_w, s + ml, s + m2, i, l), av[l * P + k2]);
-          const cplx alc = cscale(Y[c * LM_S + jj], sqrt(omega[k2]) * it);  // conj(alpha)
-          cfma(acc, alc, wa);
+            for (int l = 0; l < P; ++l)
+              cfma(wa, wget<P>(W, n_w, s + ml, s + m2, i, l), av[l * P + k2]);
+            const cplx alc = cscale(Y[c * LM_S + jj], sqrt(omega[k2]) * it);  // conj(alpha)
+            cfma(acc, alc, wa);
+          }
+          acc.x = warp_sum(acc.x);
+          acc.y = warp_sum(acc.y);
+          if (lane == 0) cmall[(tb * P + i) * LM_KBMAX + jj] = acc;
         }
-        acc.x = warp_sum(acc.x);
-        acc.y = warp_sum(acc.y);
-        if (lane == 0) cmall[(tb * P + i) * LM_KBMAX + jj] = acc;
+        __syncthreads();
+      }
+      // E_t[i, (m', l)] = Q1[i, l] [m' = ml] - sum_i2 Q2[i, i2] sum_j C_t[i2, j] gamma[(m' l), j]
+      for (int64_t e = tid; e < (int64_t)ntw * P * nwp; e += NT) {
+        const int tb = (int)(e / (P * nwp));
+        const int rem = (int)(e - (int64_t)tb * P * nwp), i = rem / nwp, col = rem - i * nwp;
+        const int m2 = col / P, l = col - m2 * P;
+        const int ml = (int)(c0 + tb - s_abs);
+        cplx x = m2 == ml ? Q1[i * P + l] : cmk(0, 0);
+        if (kb > 0) {
+          cplx dl = cmk(0, 0);
+          for (int i2 = 0; i2 < P; ++i2) {
+            cplx cg = cmk(0, 0);
+            for (int jj = 0; jj < kb; ++jj)
+              cfma(cg, cmall[(tb * P + i2) * LM_KBMAX + jj], gam[col * LM_KBMAX + jj]);
+            cfma(dl, Q2[i * P + i2], cg);
+          }
+          x = csub(x, dl);
+        }
+        Eout[(size_t)(c0 + tb - g.lo) * P * nwp + rem] = x;
       }
       __syncthreads();
     }
-    // E_t[i, (m', l)] = Q1[i, l] [m' = ml] - sum_i2 Q2[i, i2] sum_j C_t[i2, j] gamma[(m' l), j]
-    for (int64_t e = tid; e < (int64_t)ntw * P * nwp; e += NT) {
-      const int tb = (int)(e / (P * nwp));
-      const int rem = (int)(e - (int64_t)tb * P * nwp), i = rem / nwp, col = rem - i * nwp;
-      const int m2 = col / P, l = col - m2 * P;
-      const int ml = (int)(t0 + tb - s_abs);
-      cplx x = m2 == ml ? Q1[i * P + l] : cmk(0, 0);
-      if (kb > 0) {
-        cplx dl = cmk(0, 0);
-        for (int i2 = 0; i2 < P; ++i2) {
-          cplx cg = cmk(0, 0);
-          for (int jj = 0; jj < kb; ++jj)
-            cfma(cg, cmall[(tb * P + i2) * LM_KBMAX + jj], gam[col * LM_KBMAX + jj]);
-          cfma(dl, Q2[i * P + i2], cg);
-        }
-        x = csub(x, dl);
-      }
-      Eout[(size_t)(t0 + tb - g.lo) * P * nwp + rem] = x;
-    }
-    __syncthreads();
     if (tid == 0) {
       inf[0] = 0;
       inf[1] = zero_s ? 0 : iters;

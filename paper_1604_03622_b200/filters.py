@@ -15,6 +15,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 
 from . import _native as nat
@@ -305,8 +307,11 @@ def _host_grid_args(filt, dopplers, spatial_grid):
     return dop, grid
 
 
-def run_detect(filt, cube, dop, grid, groups=1):
-    """kst_detect -> device tensor (groups, n, D) float64."""
+def run_detect(filt, cube, dop, grid, groups=1, precision=None):
+    """kst_detect -> device tensor (groups, n, D) float64. `precision`
+    ("f32"/"f64") overrides the context's K5 precision for this call; the
+    optimal kind always detects in FP64 (its whitened bins feed the SINR
+    analysis of src/filters.py:185-198, not the hot path)."""
     import torch
     shp = tuple(cube.shape) if hasattr(cube, "shape") else np.shape(cube)
     if len(shp) != 3 or shp[1:] != (filt.p, filt.q):
@@ -321,11 +326,23 @@ def run_detect(filt, cube, dop, grid, groups=1):
     n, D, G = shp[0], dop.size, grid.shape[0]
     vals = torch.empty((groups, n, D), dtype=torch.float64, device=x.device)
     c = nat.ctx(x.device)
-    nat.check(nat.lib().kst_detect(
-        c, nat.ptr(x), n, filt.p, filt.q, nat.ptr(ua), 0 if ua is None else ua.shape[1],
-        nat.ptr(ub), 0 if ub is None else ub.shape[1], kind, int(bool(filt.spatial_only)),
-        dop.ctypes.data_as(nat.C.c_void_p), D, grid.ctypes.data_as(nat.C.c_void_p), G, groups,
-        nat.ptr(vals), nat.stream_of(x.device)), c)
+    if filt.kind == "optimal":
+        precision = "f64"
+    prev = None
+    if precision is not None:
+        b = C.c_int(0)
+        nat.check(nat.lib().kst_get_detect(c, C.byref(b)), c)
+        prev = b.value
+        nat.check(nat.lib().kst_set_detect(c, {"f32": 32, "f64": 64}[precision]), c)
+    try:
+        nat.check(nat.lib().kst_detect(
+            c, nat.ptr(x), n, filt.p, filt.q, nat.ptr(ua), 0 if ua is None else ua.shape[1],
+            nat.ptr(ub), 0 if ub is None else ub.shape[1], kind, int(bool(filt.spatial_only)),
+            dop.ctypes.data_as(nat.C.c_void_p), D, grid.ctypes.data_as(nat.C.c_void_p), G, groups,
+            nat.ptr(vals), nat.stream_of(x.device)), c)
+    finally:
+        if prev is not None:
+            nat.lib().kst_set_detect(c, prev)
     return vals
 
 
@@ -337,3 +354,22 @@ def detection_image(filt, cube, dopplers, spatial_grid, pool=None):
     dop, grid = _host_grid_args(filt, dopplers, spatial_grid)
     vals = run_detect(filt, cube, dop, grid)[0]
     return DetectionMap(vals if nat.is_device(cube) else nat.to_host(vals), dop, grid)
+
+
+def set_detect_precision(precision="f32", device=None):
+    """Select the detection (K5) arithmetic for this thread's context:
+    "f32" (default: FP64 load pass -- spatial reduction and temporal
+    coefficients -- then an FP32 prime-factor Doppler transform and pixel
+    stage, within the SURVEY.md §8c map comparator; single-map uniform-grid
+    cases, the rest run in FP64) or "f64" (FP64 kernels everywhere; maps to
+    ~1e-12 of the reference)."""
+    c = nat.ctx(device)
+    bits = {"f32": 32, "f64": 64}[precision]
+    nat.check(nat.lib().kst_set_detect(c, bits), c)
+
+
+def get_detect_precision(device=None):
+    c = nat.ctx(device)
+    b = C.c_int(0)
+    nat.check(nat.lib().kst_get_detect(c, C.byref(b)), c)
+    return "f32" if b.value == 32 else "f64"

@@ -150,7 +150,10 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
             grids["dop"], grids["grid"] = _host_grid_args(filt, dopplers, spatial_grid)
         t0, t1 = window_bins(s, n_w, n_bins)
         t0, t1 = max(t0, lo), min(t1, hi)
-        vals[t0 - lo:t1 - lo] = run_detect(filt, x[t0 - a:t1 - a], grids["dop"], grids["grid"])[0]
+        # L-mode detects in FP64 on every path (the batched lm_detect_kernel
+        # and kst_windowed do)
+        vals[t0 - lo:t1 - lo] = run_detect(filt, x[t0 - a:t1 - a], grids["dop"], grids["grid"],
+                                           precision="f64")[0]
         if return_estimates:
             ests[s] = est
 
@@ -159,6 +162,24 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
     # stream and kst context (one ctx per device and thread, include/kst_b200.h),
     # so the small per-window kernels and host round trips of different
     # windows overlap. Every window is computed exactly as in the serial loop.
+    # Window Grams run on the FP64 DMMA engine on every path (kst_windowed
+    # and the batched kst_lmode do: the CRT engine's 2^-32 column rounding can
+    # lift a window's null b eigenvalues to the 1e-9 keep threshold)
+    caller_engine = get_gram_engine(x.device)
+    engine = ("dmma", caller_engine[1])
+    set_gram_engine(*engine, device=x.device)
+    try:
+        _run_windows(starts, workers, one_window, run_fused, fused, x, engine)
+    finally:
+        set_gram_engine(*caller_engine, device=x.device)
+    dop, grid = grids["dop"], grids["grid"]
+    ests = [(s, ests[s]) for s in starts] if return_estimates else []
+    dmap = DetectionMap(vals if dev_out else nat.to_host(vals), dop, grid)
+    return (dmap, ests) if return_estimates else dmap
+
+
+def _run_windows(starts, workers, one_window, run_fused, fused, x, engine):
+    import torch
     one_window(starts[0])
     rest = starts[1:]
     nw = max(1, min(int(workers), len(rest)))
@@ -167,7 +188,6 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
             one_window(s)
     else:
         main = torch.cuda.current_stream(x.device)
-        engine = get_gram_engine(x.device)  # the caller's K1 engine, for every worker
         pool = _pool(nw)
         local = _local
 
@@ -193,7 +213,3 @@ def windowed_detection_image(cube, n_w, rank_spatial, rank_temporal, dopplers, s
         done = [f.result() for f in futs]  # re-raises a worker's exception here
         for st in done:
             main.wait_stream(st)
-    dop, grid = grids["dop"], grids["grid"]
-    ests = [(s, ests[s]) for s in starts] if return_estimates else []
-    dmap = DetectionMap(vals if dev_out else nat.to_host(vals), dop, grid)
-    return (dmap, ests) if return_estimates else dmap

@@ -48,6 +48,47 @@ PIPELINE_CASES = ["readme_q16"] + [f"sweep_q64_ra{a}_rb{b}" for a in (1, 2, 3) f
     "classical_q64", "droptemporal_q64", "cfg1_q256"]
 
 
+@pytest.fixture(autouse=True)
+def _detection_precision_default():
+    """Every test starts from the library default K5 precision (f32) on this
+    thread's context and leaves it there, whatever it selected."""
+    yield
+    if "paper_1604_03622_b200" in sys.modules:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                sys.modules["paper_1604_03622_b200"].set_detect_precision("f32")
+        except Exception:  # pragma: no cover - no GPU / library
+            pass
+
+
+@pytest.fixture
+def f64_detection():
+    """Run the test with the FP64 detection kernels (tight parity)."""
+    import paper_1604_03622_b200 as kst
+    kst.set_detect_precision("f64")
+    yield
+    kst.set_detect_precision("f32")
+
+
+@pytest.fixture(params=["f64", "f32"])
+def precision(request):
+    """Parametrise a test over the two K5 precisions; yields the name."""
+    import paper_1604_03622_b200 as kst
+    kst.set_detect_precision(request.param)
+    yield request.param
+    kst.set_detect_precision("f32")
+
+
+def tight_tolerance(ref, m0, precision):
+    """Per-precision regression bound, far inside the SURVEY.md §8c rule:
+    FP64 detection 1e-9 |v_ref| + 1e-10 M0; FP32 detection (FP32 transform
+    of the spectra, measured max |err| <= 5e-8 M0) 1e-5 |v_ref| + 1e-6 M0."""
+    if precision == "f64":
+        return map_tolerance(ref, m0, 1e-9, 1e-10)
+    return map_tolerance(ref, m0, 1e-5, 1e-6)
+
+
 def map_tolerance(ref, m0, rel=1e-4, floor=1e-5):
     """SURVEY.md §8c map rule: |v - v_ref| <= rel*|v_ref| + floor*M0."""
     return rel * np.abs(ref) + floor * m0

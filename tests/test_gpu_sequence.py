@@ -10,7 +10,7 @@ import sys
 import numpy as np
 import pytest
 
-from conftest import ROOT, map_tolerance
+from conftest import ROOT, map_tolerance, tight_tolerance
 
 pytestmark = pytest.mark.gpu
 
@@ -49,7 +49,7 @@ def test_process_sequence_mixed_inputs_match_oracle():
     for k, (ref, m0) in enumerate(_oracle_maps(frames)):
         err = np.abs(got[k] - ref)
         assert np.all(err <= map_tolerance(ref, m0))
-        assert np.all(err <= 1e-9 * np.abs(ref) + 1e-10 * m0), f"frame {k}"
+        assert np.all(err <= tight_tolerance(ref, m0, "f32")), f"frame {k}"  # default precision
 
 
 def test_process_sequence_torchrun_nccl_gather(tmp_path):
@@ -64,4 +64,4 @@ def test_process_sequence_torchrun_nccl_gather(tmp_path):
     got = np.load(out)
     assert got.shape == (3, Q, Q)
     for k, (ref, m0) in enumerate(_oracle_maps(_frames(3))):
-        assert np.all(np.abs(got[k] - ref) <= 1e-9 * np.abs(ref) + 1e-10 * m0)
+        assert np.all(np.abs(got[k] - ref) <= tight_tolerance(ref, m0, "f32"))

@@ -49,6 +49,20 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
 
 namespace {
 
+#ifdef KST_LM_PROF
+// phase clock stamps of every window (A/B builds only: -DKST_LM_PROF)
+__device__ long long lm_prof[4096][16];
+#define LM_STAMP(w, k) \
+  do {                 \
+    __syncthreads();   \
+    if (threadIdx.x == 0 && (w) < 4096) lm_prof[w][k] = clock64(); \
+  } while (0)
+#else
+#define LM_STAMP(w, k) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr int LM_NWMAX = 128;  // training window of the batched path
 constexpr int LM_KBMAX = 6;    // temporal basis width of the batched path
 constexpr int LM_S = 8;        // subspace block
@@ -176,6 +190,65 @@ __global__ void band_reduce_kernel(const cplx* __restrict__ Wp, int nsplit, int6
       for (int k = 0; k < nsplit; ++k) acc = cadd(acc, rsp[k * rcount + r]);
       rs[r] = acc;
     }
+  }
+}
+
+// Band-prefix record rows: for bin m and length L = 1..n_w,
+//   Qp[m][L-1] = sum_{o < L} g(m, o),  g(m, o) = the record contribution of the
+//   pair (m, m + o): [(o ? 2 : 1) |tr B|^2, #non-finite entries of B,
+//   M upper triangle re/im: B[i,k] conj(B[j,l]) (+ conj(B[k,i]) B[l,j] for o > 0)]
+// with B = W_{m, m+o}. A window [s, s + n_w) owns exactly the pairs
+// (s + ml, s + ml + o), o < n_w - ml, so its record is the sum of the n_w rows
+// Qp[s + ml][n_w - ml - 1] -- n_w row reads instead of n_w (n_w + 1) / 2 pair
+// products per window (consecutive windows share all but 2 n_w - 1 pairs).
+// Thread = (bin, record item); W blocks of a bin are shared through L1.
+template <int P>
+__global__ void __launch_bounds__(256) band_prefix_kernel(const cplx* __restrict__ W, int nb, int n_w,
+                                                          double* __restrict__ Qp) {
+  constexpr int U = P * P, E = U * (U + 1) / 2, NQ = 2 + 2 * E, NI = 2 + E;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (int64_t)nb * NI) return;
+  const int m = (int)(gid / NI), it = (int)(gid - (int64_t)m * NI);
+  double* out = Qp + (int64_t)m * n_w * NQ;
+  const cplx* wm = W + (int64_t)m * n_w * U;
+  if (it < 2) {
+    double acc = 0.0;
+    for (int o = 0; o < n_w; ++o) {
+      if (m + o < nb) {
+        const cplx* B = wm + (int64_t)o * U;
+        if (it == 0) {
+          cplx tr = cmk(0, 0);
+#pragma unroll
+          for (int i = 0; i < P; ++i) tr = cadd(tr, B[i * P + i]);
+          acc = fma(o ? 2.0 : 1.0, cabs2(tr), acc);
+        } else {
+#pragma unroll
+          for (int k = 0; k < U; ++k) acc += (isfinite(B[k].x) && isfinite(B[k].y)) ? 0.0 : 1.0;
+        }
+      }
+      out[(int64_t)o * NQ + it] = acc;
+    }
+    return;
+  }
+  // upper-triangle entry e2 = it - 2 -> (u, x), u <= x
+  int u = 0, rem = it - 2;
+  while (rem >= U - u) {
+    rem -= U - u;
+    ++u;
+  }
+  const int x = u + rem;
+  const int i = u / P, j = u % P, k = x / P, l = x % P;
+  cplx acc = cmk(0, 0);
+  for (int o = 0; o < n_w; ++o) {
+    if (m + o < nb) {
+      const cplx* B = wm + (int64_t)o * U;
+      cplx t = cmulc(B[i * P + k], B[j * P + l]);
+      if (o) t = cadd(t, cmulc(B[l * P + j], B[k * P + i]));
+      acc.x += t.x;
+      acc.y += t.y;
+    }
+    out[(int64_t)o * NQ + 2 + 2 * (it - 2)] = acc.x;
+    out[(int64_t)o * NQ + 3 + 2 * (it - 2)] = acc.y;
   }
 }
 
@@ -344,7 +417,8 @@ constexpr int WI = 8;
 
 template <int P>
 __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ W,
-                                                       const cplx* __restrict__ rs, WinArgs g,
+                                                       const cplx* __restrict__ rs,
+                                                       const double* __restrict__ Qp, WinArgs g,
                                                        cplx* __restrict__ Hscr,
                                                        double* __restrict__ resid_scr,
                                                        cplx* __restrict__ Eout,
@@ -363,7 +437,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
   cplx* gam = Z + (size_t)g.nbmax * LM_S;  // n_w P x LM_KBMAX
   cplx* cmall = gam + (size_t)g.n_w * P * LM_KBMAX;  // (n_w / 2 + 1) x P x LM_KBMAX
   __shared__ double red[4 + 2 * U + 2 * E];
-  __shared__ double recv[NREC];
+  __shared__ double recv[NREC + 1];
   __shared__ IterState st;
   __shared__ cplx spatial[kMaxP * kMaxP];
   __shared__ double dinfo[4], hdiag[8];
@@ -381,73 +455,27 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
   for (int w = blockIdx.x; w < g.nwin; w += gridDim.x) {
     const int64_t s_abs = g.s0 + w;
     const int s = (int)(s_abs - g.a);  // window's first bin in the tile cube
+    LM_STAMP(w, 0);
     // ---------------------------------------------------------- (1) record
-    // pairs (m, m') of the window's bins, band order; 4 groups of 64 threads,
-    // group gi owns M entries [gi EPG, (gi + 1) EPG) (+ |S|_F^2 in group 0);
-    // each thread strides the pairs; fixed-order reductions (deterministic)
+    // the window's pairs (m, m'), m <= m' in [s, s + n_w): for each of its
+    // bins m = s + ml the offsets o < n_w - ml, i.e. the band-prefix row
+    // Qp[m][n_w - ml - 1] (band_prefix_kernel); thread = record slot, the
+    // n_w rows summed in bin order (deterministic, tile-independent)
     {
-      constexpr int NGR = 4, EPG = (E + NGR - 1) / NGR, NV = 1 + 2 * EPG;
-      const int gi = tid / (NT / NGR), gt = tid % (NT / NGR);
-      double v[NV];
-#pragma unroll
-      for (int k = 0; k < NV; ++k) v[k] = 0.0;
-      int bad = 0;
-      for (int e = gt; e < n_w * n_w; e += NT / NGR) {
-        const int ml = e / n_w, o = e - ml * n_w;
-        if (o >= n_w - ml) continue;
-        const cplx* bp = W + ((int64_t)(s + ml) * n_w + o) * NPW;
-        cplx B[NPW];
-#pragma unroll
-        for (int k = 0; k < NPW; ++k) {
-          B[k] = bp[k];
-          if (!isfinite(B[k].x) || !isfinite(B[k].y)) bad = 1;
-        }
-        if (gi == 0) {
-          cplx tr = cmk(0, 0);
-#pragma unroll
-          for (int i = 0; i < P; ++i) tr = cadd(tr, B[i * P + i]);
-          v[0] = fma(o ? 2.0 : 1.0, cabs2(tr), v[0]);
-        }
-        // M[(i,j),(k,l)] += B[i,k] conj(B[j,l]) (+ the mirrored pair's conj(B[k,i]) B[l,j])
-        int e2 = 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int x = u; x < U; ++x, ++e2) {
-            if (e2 / EPG != gi) continue;
-            const int i = u / P, j = u % P, k = x / P, l = x % P;
-            cplx t = cmulc(B[i * P + k], B[j * P + l]);
-            if (o) t = cadd(t, cmulc(B[l * P + j], B[k * P + i]));
-            v[1 + 2 * (e2 % EPG)] += t.x;
-            v[2 + 2 * (e2 % EPG)] += t.y;
-          }
-      }
-      bad = __syncthreads_or(bad);
-      const int wid = tid >> 5, lane = tid & 31;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const double x = warp_sum(v[k]);
-        if (lane == 0) scratch[wid * NV + k] = x;
-      }
-      __syncthreads();
-      constexpr int WPG = NT / NGR / 32;  // warps per group
-      for (int k = tid; k < NGR * NV; k += NT) {
-        const int g2 = k / NV, kv = k - g2 * NV;
+      constexpr int NQ = 2 + 2 * E;
+      for (int k = tid; k < NQ; k += NT) {
         double x = 0.0;
-        for (int ww = 0; ww < WPG; ++ww) x += scratch[(g2 * WPG + ww) * NV + kv];
-        if (kv == 0) {
-          if (g2 == 0) recv[0] = x;
-        } else {
-          const int ent = g2 * EPG + ((kv - 1) >> 1);
-          if (ent < E) recv[1 + 2 * ent + ((kv - 1) & 1)] = x;
-        }
+#pragma unroll 8
+        for (int ml = 0; ml < n_w; ++ml)
+          x += Qp[((int64_t)(s + ml) * n_w + (n_w - 1 - ml)) * NQ + k];
+        recv[k] = x;
       }
       __syncthreads();
       const double inv_n2 = 1.0 / (nn * nn);
       for (int k = tid; k < 4 + 2 * U + 2 * E; k += NT) {
         double x;
         if (k == 0) x = recv[0] * inv_n2;
-        else if (k == 1) x = bad ? 1.0 : 0.0;
+        else if (k == 1) x = recv[1] != 0.0 ? 1.0 : 0.0;  // non-finite window data
         else if (k == 2) x = 0.0;  // window S diagonal = (1/n) sum |x|^2 >= 0
         else if (k == 3) x = 1.0;
         else if (k < 4 + 2 * U) {
@@ -458,12 +486,13 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
             cfmac(acc, rs[(int64_t)(s + ml) * P + i], rs[(int64_t)(s + ml) * P + j]);
           x = ((k - 4) & 1 ? acc.y : acc.x) / nn;
         } else {
-          x = recv[1 + (k - 4 - 2 * U)] * inv_n2;
+          x = recv[2 + (k - 4 - 2 * U)] * inv_n2;
         }
         red[k] = x;
       }
       __syncthreads();
     }
+    LM_STAMP(w, 1);
     // ---------------------------------------------------------- (2) LR-Kron iterations
     double* resid = resid_scr + (size_t)blockIdx.x * (g.max_iter + 1);
     m_iterations<P>(red, g.q, g.ra, g.tol, g.max_iter, &st, jsm, spatial, resid, dinfo, hdiag);
@@ -491,6 +520,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
       }
       continue;
     }
+    LM_STAMP(w, 2);
     // ---------------------------------------------------------- (3) U_A = subspace_basis(A)
     if (!zero_s) {
       JacSmem j = jac_carve(jsm, P);
@@ -547,6 +577,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
       }
       continue;
     }
+    LM_STAMP(w, 3);
     // ---------------------------------------------------------- (5) H and its top pairs
     const int kk = zero_s ? 0 : min(g.rb, nb);
     cplx* H = Hscr + (size_t)blockIdx.x * g.nbmax * g.nbmax;
@@ -566,6 +597,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
         H[e] = cscale(acc, sqrt(omega[k1] * omega[k2]));
       }
       __syncthreads();
+      LM_STAMP(w, 4);
       if (nb <= LM_JAC) {
         JacSmem j = jac_carve(jsm, nb);
         jac_solve(j, H, nb, nb, 1.0);
@@ -577,21 +609,39 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
         __syncthreads();
       } else {
         const int sb = min(LM_S, nb);
-        // start block: unit vectors at the sb largest diagonal entries (ties: lower index)
-        if (tid == 0) {
+        // start block: unit vectors at the sb largest diagonal entries (ties:
+        // lower index); warp 0, lane l holds rows l + 32 i (nb <= LM_NBMAX),
+        // sb rounds of a warp argmax
+        if (tid < 32) {
+          constexpr int RPL = LM_NBMAX / 32;
+          double dv[RPL];
+#pragma unroll
+          for (int i = 0; i < RPL; ++i) {
+            const int row = tid + 32 * i;
+            dv[i] = row < nb ? H[(int64_t)row * nb + row].x : -INFINITY;
+          }
           for (int k = 0; k < sb; ++k) {
-            int best = -1;
-            double bv = -1e308;
-            for (int i2 = 0; i2 < nb; ++i2) {
-              bool used = false;
-              for (int k2 = 0; k2 < k; ++k2) used |= sel[k2] == i2;
-              const double dv = H[(int64_t)i2 * nb + i2].x;
-              if (!used && dv > bv) {
-                bv = dv;
-                best = i2;
+            double bv = -INFINITY;
+            int bi = nb;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i)
+              if (dv[i] > bv) {
+                bv = dv[i];
+                bi = tid + 32 * i;
+              }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+              if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
               }
             }
-            sel[k] = best;
+            if (tid == 0) sel[k] = bi;
+#pragma unroll
+            for (int i = 0; i < RPL; ++i)
+              if (tid + 32 * i == bi) dv[i] = -INFINITY;
           }
         }
         __syncthreads();
@@ -601,21 +651,28 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
         }
         if (tid == 0) unit_s = 0;
         __syncthreads();
+        LM_STAMP(w, 14);
         bool done = false;
         int round = 0;
         double prev_worst = 1e300;
         int stall = 0;
         for (; round < LM_MAXR && !done; ++round) {
           // two power steps, each followed by CGS2 orthonormalisation
+          LM_STAMP(w, 8);
           hmul(H, nb, Y, Z, sb);
+          LM_STAMP(w, 9);
           cgs2(Z, nb, sb, coefs, nrm2, &unit_s);
+          LM_STAMP(w, 10);
           hmul(H, nb, Z, Y, sb);
           cgs2(Y, nb, sb, coefs, nrm2, &unit_s);
           if (round < 1) continue;  // H^4 warm-up before the first Rayleigh-Ritz
+          LM_STAMP(w, 11);
           hmul(H, nb, Y, Z, sb);
           block_gram(Y, Z, nb, sb, G8);  // T = Y^H H Y
+          LM_STAMP(w, 12);
           JacSmem j = jac_carve(jsm, sb);
           jac_solve(j, G8, LM_S, sb, 1.0);
+          LM_STAMP(w, 13);
           rotate_block(Y, nb, sb, j);
           rotate_block(Z, nb, sb, j);
           if (tid < sb) theta[tid] = j.val[j.order[tid]];
@@ -684,6 +741,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
       }
       __syncthreads();
     }
+    LM_STAMP(w, 5);
     // ---------------------------------------------------------- (7) filter kind -> Q1, Q2
     if (tid == 0) {
       const bool has_a = ka_s > 0, has_b = kb_s > 0;
@@ -725,6 +783,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
       }
       __syncthreads();
     }
+    LM_STAMP(w, 6);
     // ---------------------------------------------------------- (8) E for the window's test bins
     const int h = n_w / 2;
     int64_t t0 = (s_abs == 0) ? 0 : s_abs + h;
@@ -740,49 +799,76 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
       const int ntw = (int)(c1 - c0);
       if (kb > 0 && ntw > 0) {
         // C_t[i, j] = sum_{m'k'} conj(alpha[(m'k'), j]) (W_{ml m'} a_k')[i], all test bins:
-        // warp per (bin, i, j) output, lanes stride the n_w r window columns
+        // warp per test bin, lanes stride the n_w r window columns; each lane
+        // reads its W block once for all (i, j) (P x kb accumulators); per
+        // (i, j) the same lane order and warp_sum tree as a per-output warp
         const int wid = tid >> 5, lane = tid & 31;
-        for (int o = wid; o < ntw * P * kb; o += NT / 32) {
-          const int tb = o / (P * kb), rem = o - tb * P * kb, i = rem / kb, jj = rem - i * kb;
+        for (int tb = wid; tb < ntw; tb += NT / 32) {
           const int ml = (int)(c0 + tb - s_abs);
-          const double it = 1.0 / sqrt(theta[jj]);
-          cplx acc = cmk(0, 0);
+          cplx acc[P][LM_KBMAX];
+#pragma unroll
+          for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int jj = 0; jj < LM_KBMAX; ++jj) acc[i][jj] = cmk(0, 0);
           for (int c = lane; c < nb; c += 32) {
             const int m2 = c / r, k2 = c - m2 * r;
-            cplx wa = cmk(0, 0);
+            cplx wa[P];
 #pragma unroll
-            for (int l = 0; l < P; ++l)
-              cfma(wa, wget<P>(W, n_w, s + ml, s + m2, i, l), av[l * P + k2]);
-            const cplx alc = cscale(Y[c * LM_S + jj], sqrt(omega[k2]) * it);  // conj(alpha)
-            cfma(acc, alc, wa);
+            for (int i = 0; i < P; ++i) {
+              wa[i] = cmk(0, 0);
+#pragma unroll
+              for (int l = 0; l < P; ++l)
+                cfma(wa[i], wget<P>(W, n_w, s + ml, s + m2, i, l), av[l * P + k2]);
+            }
+            const double so = sqrt(omega[k2]);
+#pragma unroll
+            for (int jj = 0; jj < LM_KBMAX; ++jj) {
+              if (jj >= kb) break;
+              const cplx alc = cscale(Y[c * LM_S + jj], so * (1.0 / sqrt(theta[jj])));  // conj(alpha)
+#pragma unroll
+              for (int i = 0; i < P; ++i) cfma(acc[i][jj], alc, wa[i]);
+            }
           }
-          acc.x = warp_sum(acc.x);
-          acc.y = warp_sum(acc.y);
-          if (lane == 0) cmall[(tb * P + i) * LM_KBMAX + jj] = acc;
+#pragma unroll
+          for (int i = 0; i < P; ++i)
+#pragma unroll
+            for (int jj = 0; jj < LM_KBMAX; ++jj) {
+              if (jj >= kb) break;
+              const double ax = warp_sum(acc[i][jj].x), ay = warp_sum(acc[i][jj].y);
+              if (lane == 0) cmall[(tb * P + i) * LM_KBMAX + jj] = cmk(ax, ay);
+            }
         }
         __syncthreads();
       }
       // E_t[i, (m', l)] = Q1[i, l] [m' = ml] - sum_i2 Q2[i, i2] sum_j C_t[i2, j] gamma[(m' l), j]
-      for (int64_t e = tid; e < (int64_t)ntw * P * nwp; e += NT) {
-        const int tb = (int)(e / (P * nwp));
-        const int rem = (int)(e - (int64_t)tb * P * nwp), i = rem / nwp, col = rem - i * nwp;
+      // thread = window column (m', l) with its gamma row in registers, all
+      // (test bin, channel) rows; stores coalesced over the columns
+      for (int col = tid; col < nwp; col += NT) {
         const int m2 = col / P, l = col - m2 * P;
-        const int ml = (int)(c0 + tb - s_abs);
-        cplx x = m2 == ml ? Q1[i * P + l] : cmk(0, 0);
-        if (kb > 0) {
-          cplx dl = cmk(0, 0);
-          for (int i2 = 0; i2 < P; ++i2) {
-            cplx cg = cmk(0, 0);
-            for (int jj = 0; jj < kb; ++jj)
-              cfma(cg, cmall[(tb * P + i2) * LM_KBMAX + jj], gam[col * LM_KBMAX + jj]);
-            cfma(dl, Q2[i * P + i2], cg);
+        cplx gv[LM_KBMAX];
+#pragma unroll
+        for (int jj = 0; jj < LM_KBMAX; ++jj) gv[jj] = jj < kb ? gam[col * LM_KBMAX + jj] : cmk(0, 0);
+        for (int row = 0; row < ntw * P; ++row) {
+          const int tb = row / P, i = row - tb * P;
+          const int ml = (int)(c0 + tb - s_abs);
+          cplx x = m2 == ml ? Q1[i * P + l] : cmk(0, 0);
+          if (kb > 0) {
+            cplx dl = cmk(0, 0);
+            for (int i2 = 0; i2 < P; ++i2) {
+              cplx cg = cmk(0, 0);
+#pragma unroll
+              for (int jj = 0; jj < LM_KBMAX; ++jj)
+                if (jj < kb) cfma(cg, cmall[(tb * P + i2) * LM_KBMAX + jj], gv[jj]);
+              cfma(dl, Q2[i * P + i2], cg);
+            }
+            x = csub(x, dl);
           }
-          x = csub(x, dl);
+          Eout[(size_t)(c0 + tb - g.lo) * P * nwp + (size_t)i * nwp + col] = x;
         }
-        Eout[(size_t)(c0 + tb - g.lo) * P * nwp + rem] = x;
       }
       __syncthreads();
     }
+    LM_STAMP(w, 7);
     if (tid == 0) {
       inf[0] = 0;
       inf[1] = zero_s ? 0 : iters;
@@ -917,11 +1003,20 @@ int launch_band(kst_ctx* ctx, const cplx* X, int nb, int q, int n_w, cplx* W, cp
 }
 
 template <int P>
-int launch_win(kst_ctx* ctx, const cplx* W, const cplx* rs, const WinArgs& wa, cplx* H,
-               double* rscr, cplx* E, int* dinfo, double* dres, size_t wsm, cudaStream_t st) {
+int launch_prefix(kst_ctx* ctx, const cplx* W, int nb, int n_w, double* Qp, cudaStream_t st) {
+  constexpr int NI = 2 + P * P * (P * P + 1) / 2;
+  band_prefix_kernel<P><<<(unsigned)cdiv((int64_t)nb * NI, 256), 256, 0, st>>>(W, nb, n_w, Qp);
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}
+
+template <int P>
+int launch_win(kst_ctx* ctx, const cplx* W, const cplx* rs, const double* Qp, const WinArgs& wa,
+               cplx* H, double* rscr, cplx* E, int* dinfo, double* dres, size_t wsm,
+               cudaStream_t st) {
   KST_CUDA(ctx, cudaFuncSetAttribute(window_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)wsm));
-  window_kernel<P><<<wa.nslot, NT, wsm, st>>>(W, rs, wa, H, rscr, E, dinfo, dres);
+  window_kernel<P><<<wa.nslot, NT, wsm, st>>>(W, rs, Qp, wa, H, rscr, E, dinfo, dres);
   KST_LAUNCH(ctx);
   return KST_OK;
 }
@@ -937,6 +1032,12 @@ int launch_det(kst_ctx* ctx, const cplx* spec, const cplx* E, const cplx* hconj,
 }
 
 }  // namespace
+
+#ifdef KST_LM_PROF
+extern "C" __attribute__((visibility("default"))) int kst_lm_prof(long long* out, int nwin) {
+  return (int)cudaMemcpyFromSymbol(out, lm_prof, sizeof(long long) * 16 * std::min(nwin, 4096));
+}
+#endif
 
 extern "C" int kst_windowed(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_bins, int p,
                             int q, int n_w, int64_t lo, int64_t hi, int64_t s_begin, int64_t s_end,
@@ -994,8 +1095,12 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
                                                    sizeof(double) * D + 256);
   const int nsplit = band_splits(q);
   // W + row sums, then (split-K) nsplit partial copies of both
-  char* wW = (char*)ws_get(ctx, WS_LM_W, sizeof(cplx) * ((size_t)nb * n_w * p * p + (size_t)nb * p) *
-                                             (nsplit > 1 ? nsplit + 1 : 1) + 256);
+  // band-prefix record rows (nb x n_w x (2 + 2E) doubles), then W + row sums,
+  // then (split-K) nsplit partial copies of both
+  const size_t nq = 2 + (size_t)p * p * (p * p + 1);
+  const size_t qbytes = (sizeof(double) * (size_t)nb * n_w * nq + 255) / 256 * 256;
+  char* wW = (char*)ws_get(ctx, WS_LM_W, qbytes + sizeof(cplx) * ((size_t)nb * n_w * p * p + (size_t)nb * p) *
+                                                      (nsplit > 1 ? nsplit + 1 : 1) + 256);
   char* wE = (char*)ws_get(ctx, WS_LM_E, sizeof(cplx) * (size_t)n_test * p * nwp +
                                              sizeof(int) * (size_t)nwin * WI + sizeof(double) * nwin + 256);
   char* wH = (char*)ws_get(ctx, WS_LM_H, sizeof(cplx) * (size_t)nslot * nbmax * nbmax +
@@ -1005,7 +1110,8 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   cplx* spec = (cplx*)wspec;
   cplx* hconj = spec + (size_t)nb * p * D;
   void* consts = hconj + (size_t)G * p;
-  cplx* W = (cplx*)wW;
+  double* Qp = (double*)wW;
+  cplx* W = (cplx*)(wW + qbytes);
   cplx* rs = W + (size_t)nb * n_w * p * p;
   cplx* Wp = rs + (size_t)nb * p;  // split-K partials (nsplit > 1)
   cplx* E = (cplx*)wE;
@@ -1028,6 +1134,11 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
     default: KST_TRY(launch_band<3>(ctx, X, nb, q, n_w, W, rs, Wp, st)); break;
   }
   KST_LAUNCH(ctx);
+  switch (p) {
+    case 1: KST_TRY(launch_prefix<1>(ctx, W, nb, n_w, Qp, st)); break;
+    case 2: KST_TRY(launch_prefix<2>(ctx, W, nb, n_w, Qp, st)); break;
+    default: KST_TRY(launch_prefix<3>(ctx, W, nb, n_w, Qp, st)); break;
+  }
   // 3. one CTA per window (persistent over nslot CTAs)
   WinArgs wa;
   wa.a = a;
@@ -1048,9 +1159,9 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   wa.tol = tol;
   const size_t wsm = window_smem(nbmax, n_w, p);
   switch (p) {
-    case 1: KST_TRY(launch_win<1>(ctx, W, rs, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
-    case 2: KST_TRY(launch_win<2>(ctx, W, rs, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
-    default: KST_TRY(launch_win<3>(ctx, W, rs, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
+    case 1: KST_TRY(launch_win<1>(ctx, W, rs, Qp, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
+    case 2: KST_TRY(launch_win<2>(ctx, W, rs, Qp, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
+    default: KST_TRY(launch_win<3>(ctx, W, rs, Qp, wa, H, rscr, E, dinfo, dres, wsm, st)); break;
   }
   KST_LAUNCH(ctx);
   // 4. detection of the tile's test bins

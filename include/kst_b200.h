@@ -29,6 +29,7 @@
 #ifndef KST_B200_H
 #define KST_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -55,6 +56,19 @@ int kst_ctx_create(int device, kst_ctx** out);
 int kst_ctx_destroy(kst_ctx* ctx);
 const char* kst_last_error(const kst_ctx* ctx);
 int kst_version(void);
+
+/*
+ * Pageable host <-> device copy (the boundary the reference's numpy inputs
+ * cross; the reference itself never leaves the host): `bytes` from src to
+ * dst through a ring of 4 MB pinned staging chunks filled / drained by
+ * `threads` host threads while the copy engine moves the other chunks
+ * (~33 GB/s from pageable numpy memory on the B200 box vs ~11 GB/s for a
+ * plain pageable cudaMemcpy). dir 0: host src -> dev dst, enqueued on
+ * `stream` (src may be reused on return); dir 1: dev src -> host dst,
+ * complete on return.
+ */
+int kst_copy_staged(kst_ctx* ctx, void* dst, const void* src, size_t bytes, int dir, int threads,
+                    void* stream);
 
 /* Instrumentation (bench/profiling only; no effect on results):
  * kst_launch_count: kernels launched by this context so far.

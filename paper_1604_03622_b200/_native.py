@@ -26,6 +26,7 @@ _ip = C.POINTER(C.c_int)
 
 _SIGS = {
     "kst_version": (_i, []),
+    "kst_copy_staged": (_i, [_vp, _vp, _vp, C.c_size_t, _i, _i, _vp]),
     "kst_ctx_create": (_i, [_i, C.POINTER(_vp)]),
     "kst_ctx_destroy": (_i, [_vp]),
     "kst_last_error": (C.c_char_p, [_vp]),
@@ -159,11 +160,34 @@ def to_device(x, dtype="complex128", device=None):
             t = t.to(tdt)
         return t.contiguous()
     arr = np.ascontiguousarray(np.asarray(x, dtype=np.dtype(dtype)))
-    t = torch.from_numpy(arr)
-    return t.to(device=f"cuda:{device_index(device)}", non_blocking=False)
+    dev = f"cuda:{device_index(device)}"
+    if arr.nbytes >= STAGED_MIN_BYTES:
+        # pageable numpy memory: staged through pinned chunks on several host
+        # threads (kst_copy_staged), ~3x a pageable cudaMemcpy
+        t = torch.empty(arr.shape, dtype=tdt, device=dev)
+        c = ctx(t.device)
+        check(lib().kst_copy_staged(c, ptr(t), arr.ctypes.data_as(C.c_void_p), arr.nbytes, 0,
+                                    staged_threads(), stream_of(t.device)), c)
+        return t
+    return torch.from_numpy(arr).to(device=dev, non_blocking=False)
+
+
+STAGED_MIN_BYTES = 8 << 20
+
+
+def staged_threads():
+    """Host threads of a staged copy: half the cores, 2..8."""
+    return max(2, min(8, (os.cpu_count() or 4) // 2))
 
 
 def to_host(t):
     if t is None:
         return None
-    return t.detach().cpu().numpy()
+    t = t.detach()
+    if t.is_cuda and t.is_contiguous() and t.numel() * t.element_size() >= STAGED_MIN_BYTES:
+        out = np.empty(tuple(t.shape), dtype=_torch().empty(0, dtype=t.dtype).numpy().dtype)
+        c = ctx(t.device)
+        check(lib().kst_copy_staged(c, out.ctypes.data_as(C.c_void_p), ptr(t), out.nbytes, 1,
+                                    staged_threads(), stream_of(t.device)), c)
+        return out
+    return t.cpu().numpy()

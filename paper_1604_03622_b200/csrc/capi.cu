@@ -127,6 +127,9 @@ int kst_ctx_destroy(kst_ctx* ctx) {
     for (auto& e : ctx->ev)
       if (e) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->stage) cudaFreeHost(ctx->stage);
+    for (auto& e : ctx->stage_ev)
+      if (e) cudaEventDestroy(e);
   }
   delete ctx;
   return KST_OK;

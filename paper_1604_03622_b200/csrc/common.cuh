@@ -92,6 +92,11 @@ struct kst_ctx {
   nvtxRangeId_t nvtx_stage = 0, nvtx_sub = 0;
   cudaEvent_t ev[8] = {};
   int n_ev = 0;
+  // pageable host <-> device staging ring (hostio.cu): pinned chunks and the
+  // events that guard their reuse
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev[32] = {};
 };
 
 // record stage boundary k on `st` when profiling (kst_pipeline)

@@ -479,7 +479,10 @@ __global__ void __launch_bounds__(NT, 1) mgram_reg_kernel(const cplx* __restrict
 // triangle; group 0 also owns the scans and block sums. Same partial record
 // as mgram_kernel.
 constexpr int MS_NTG = 128;  // threads per group = positions per tile
-constexpr int MS_STAGES = 4;
+#ifndef KST_MS_STAGES
+#define KST_MS_STAGES 4
+#endif
+constexpr int MS_STAGES = KST_MS_STAGES;
 // chunk bounds: group 0 (which also carries the scans) takes a smaller share
 __host__ __device__ constexpr int ms_bound(int E, int NG, int g) {
   return g <= 0 ? 0

@@ -194,61 +194,75 @@ __global__ void band_reduce_kernel(const cplx* __restrict__ Wp, int nsplit, int6
 }
 
 // Band-prefix record rows: for bin m and length L = 1..n_w,
-//   Qp[m][L-1] = sum_{o < L} g(m, o),  g(m, o) = the record contribution of the
-//   pair (m, m + o): [(o ? 2 : 1) |tr B|^2, #non-finite entries of B,
-//   M upper triangle re/im: B[i,k] conj(B[j,l]) (+ conj(B[k,i]) B[l,j] for o > 0)]
-// with B = W_{m, m+o}. A window [s, s + n_w) owns exactly the pairs
-// (s + ml, s + ml + o), o < n_w - ml, so its record is the sum of the n_w rows
-// Qp[s + ml][n_w - ml - 1] -- n_w row reads instead of n_w (n_w + 1) / 2 pair
-// products per window (consecutive windows share all but 2 n_w - 1 pairs).
-// Thread = (bin, record item); W blocks of a bin are shared through L1.
+//   Qp[m][slot][L-1] = sum_{o < L} g(m, o)[slot],  g(m, o) = the record
+//   contribution of the pair (m, m + o): [(o ? 2 : 1) |tr B|^2, #non-finite
+//   entries of B, M upper triangle re/im: B[i,k] conj(B[j,l]) (+ conj(B[k,i])
+//   B[l,j] for o > 0)] with B = W_{m, m+o}. A window [s, s + n_w) owns exactly
+//   the pairs (s + ml, s + ml + o), o < n_w - ml, so its record is the sum of
+//   the n_w entries Qp[s + ml][.][n_w - ml - 1] -- n_w reads instead of
+//   n_w (n_w + 1) / 2 pair products per window (consecutive windows share all
+//   but 2 n_w - 1 pairs). Warp per (bin, record item): lanes take offsets
+//   o = 32 c + lane, warp inclusive scan per 32-offset chunk plus the running
+//   carry (fixed shuffle tree: deterministic, tile-independent).
 template <int P>
 __global__ void __launch_bounds__(256) band_prefix_kernel(const cplx* __restrict__ W, int nb, int n_w,
                                                           double* __restrict__ Qp) {
   constexpr int U = P * P, E = U * (U + 1) / 2, NQ = 2 + 2 * E, NI = 2 + E;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (int64_t)nb * NI) return;
-  const int m = (int)(gid / NI), it = (int)(gid - (int64_t)m * NI);
-  double* out = Qp + (int64_t)m * n_w * NQ;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= (int64_t)nb * NI) return;
+  const int m = (int)(wid / NI), it = (int)(wid - (int64_t)m * NI);
   const cplx* wm = W + (int64_t)m * n_w * U;
-  if (it < 2) {
-    double acc = 0.0;
-    for (int o = 0; o < n_w; ++o) {
-      if (m + o < nb) {
-        const cplx* B = wm + (int64_t)o * U;
-        if (it == 0) {
-          cplx tr = cmk(0, 0);
-#pragma unroll
-          for (int i = 0; i < P; ++i) tr = cadd(tr, B[i * P + i]);
-          acc = fma(o ? 2.0 : 1.0, cabs2(tr), acc);
-        } else {
-#pragma unroll
-          for (int k = 0; k < U; ++k) acc += (isfinite(B[k].x) && isfinite(B[k].y)) ? 0.0 : 1.0;
-        }
-      }
-      out[(int64_t)o * NQ + it] = acc;
+  int i = 0, j = 0, k = 0, l = 0;
+  if (it >= 2) {  // upper-triangle entry it - 2 -> (u, x), u <= x
+    int u = 0, rem = it - 2;
+    while (rem >= U - u) {
+      rem -= U - u;
+      ++u;
     }
-    return;
+    const int x = u + rem;
+    i = u / P, j = u % P, k = x / P, l = x % P;
   }
-  // upper-triangle entry e2 = it - 2 -> (u, x), u <= x
-  int u = 0, rem = it - 2;
-  while (rem >= U - u) {
-    rem -= U - u;
-    ++u;
-  }
-  const int x = u + rem;
-  const int i = u / P, j = u % P, k = x / P, l = x % P;
-  cplx acc = cmk(0, 0);
-  for (int o = 0; o < n_w; ++o) {
-    if (m + o < nb) {
+  const int ns = it < 2 ? 1 : 2;  // output slots of this item
+  double* out0 = Qp + ((int64_t)m * NQ + (it < 2 ? it : 2 + 2 * (it - 2))) * n_w;
+  double carry0 = 0.0, carry1 = 0.0;
+  for (int c0 = 0; c0 < n_w; c0 += 32) {
+    const int o = c0 + lane;
+    double v0 = 0.0, v1 = 0.0;
+    if (o < n_w && m + o < nb) {
       const cplx* B = wm + (int64_t)o * U;
-      cplx t = cmulc(B[i * P + k], B[j * P + l]);
-      if (o) t = cadd(t, cmulc(B[l * P + j], B[k * P + i]));
-      acc.x += t.x;
-      acc.y += t.y;
+      if (it == 0) {
+        cplx tr = cmk(0, 0);
+#pragma unroll
+        for (int ii = 0; ii < P; ++ii) tr = cadd(tr, B[ii * P + ii]);
+        v0 = (o ? 2.0 : 1.0) * cabs2(tr);
+      } else if (it == 1) {
+#pragma unroll
+        for (int kk = 0; kk < U; ++kk) v0 += (isfinite(B[kk].x) && isfinite(B[kk].y)) ? 0.0 : 1.0;
+      } else {
+        cplx t = cmulc(B[i * P + k], B[j * P + l]);
+        if (o) t = cadd(t, cmulc(B[l * P + j], B[k * P + i]));
+        v0 = t.x;
+        v1 = t.y;
+      }
     }
-    out[(int64_t)o * NQ + 2 + 2 * (it - 2)] = acc.x;
-    out[(int64_t)o * NQ + 3 + 2 * (it - 2)] = acc.y;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // inclusive warp scan
+      const double a0 = __shfl_up_sync(0xffffffffu, v0, d);
+      const double a1 = __shfl_up_sync(0xffffffffu, v1, d);
+      if (lane >= d) {
+        v0 += a0;
+        v1 += a1;
+      }
+    }
+    v0 += carry0;
+    v1 += carry1;
+    if (o < n_w) {
+      out0[o] = v0;
+      if (ns == 2) out0[n_w + o] = v1;
+    }
+    carry0 = __shfl_sync(0xffffffffu, v0, 31);
+    carry1 = __shfl_sync(0xffffffffu, v1, 31);
   }
 }
 
@@ -458,16 +472,16 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
     LM_STAMP(w, 0);
     // ---------------------------------------------------------- (1) record
     // the window's pairs (m, m'), m <= m' in [s, s + n_w): for each of its
-    // bins m = s + ml the offsets o < n_w - ml, i.e. the band-prefix row
-    // Qp[m][n_w - ml - 1] (band_prefix_kernel); thread = record slot, the
-    // n_w rows summed in bin order (deterministic, tile-independent)
+    // bins m = s + ml the offsets o < n_w - ml, i.e. the band-prefix entry
+    // Qp[m][slot][n_w - ml - 1] (band_prefix_kernel); thread = record slot,
+    // the n_w entries summed in bin order (deterministic, tile-independent)
     {
       constexpr int NQ = 2 + 2 * E;
       for (int k = tid; k < NQ; k += NT) {
         double x = 0.0;
 #pragma unroll 8
         for (int ml = 0; ml < n_w; ++ml)
-          x += Qp[((int64_t)(s + ml) * n_w + (n_w - 1 - ml)) * NQ + k];
+          x += Qp[((int64_t)(s + ml) * NQ + k) * n_w + (n_w - 1 - ml)];
         recv[k] = x;
       }
       __syncthreads();
@@ -1004,8 +1018,8 @@ int launch_band(kst_ctx* ctx, const cplx* X, int nb, int q, int n_w, cplx* W, cp
 
 template <int P>
 int launch_prefix(kst_ctx* ctx, const cplx* W, int nb, int n_w, double* Qp, cudaStream_t st) {
-  constexpr int NI = 2 + P * P * (P * P + 1) / 2;
-  band_prefix_kernel<P><<<(unsigned)cdiv((int64_t)nb * NI, 256), 256, 0, st>>>(W, nb, n_w, Qp);
+  constexpr int NI = 2 + P * P * (P * P + 1) / 2;  // one warp per (bin, record item)
+  band_prefix_kernel<P><<<(unsigned)cdiv((int64_t)nb * NI * 32, 256), 256, 0, st>>>(W, nb, n_w, Qp);
   KST_LAUNCH(ctx);
   return KST_OK;
 }

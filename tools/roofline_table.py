@@ -24,7 +24,10 @@ DIM = P * Q
 C128 = 16
 PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
 HBM = PEAKS.get("hbm_gbs", 6548.8) * 1e9
-INT8 = 2.0 * PEAKS.get("bf16_tflops_sustained", 1376.6) * 1e12
+_I8 = os.path.join(ROOT, "profiles", "r02_int8_peak.json")
+# measured int8 dense burst peak (cuBLASLt, profiles/r02_int8_peak.json); else 2 x bf16
+INT8 = (json.load(open(_I8))["int8_dense_tops_burst"] * 1e12 if os.path.exists(_I8)
+        else 2.0 * PEAKS.get("bf16_tflops", 1608.5) * 1e12)
 FP64 = 37.0e12  # B200 FP64 (vector / DMMA) nominal; tools/fp64_peak measures it on the box
 
 # algorithmic work per launch: (kind, amount, note)
@@ -41,6 +44,8 @@ ALG = {
     "bz2_kernel": ("bytes", Q * Q * C128, "b read once"),
     "detect_bin_kernel": ("bytes", N * DIM * C128 + N * D * 8, "cube read + map written (HBM); "
                           "FP64-issue bound, DESIGN.md §4 K5"),
+    "detect_f32_kernel": ("bytes", N * DIM * C128 + N * D * 8, "cube read + map written (HBM); "
+                          "FP32 transform issue/latency bound, DESIGN.md §4 K5"),
 }
 
 
@@ -90,7 +95,7 @@ def main():
     total = sum(a[1] for a in agg.values())
     print(f"# Per-kernel roofline, one Gotcha frame (ncu --set full, cold, serialised)\n")
     print(f"HBM peak {HBM / 1e12:.2f} TB/s, int8 dense peak {INT8 / 1e12:.0f} TOP/s "
-          f"(MEASURED_PEAKS.json); frame total {total * 1e6:.0f} us over {len(order)} kernels.\n")
+          f"(profiles/r02_int8_peak.json, MEASURED_PEAKS.json); frame total {total * 1e6:.0f} us over {len(order)} kernels.\n")
     print("| kernel | calls | us | share | DRAM MB | DRAM TB/s | frac HBM | tensor % | FP64 % "
           "| ALU % | warps % | algorithmic rate | frac of its peak |")
     print("|---|---|---|---|---|---|---|---|---|---|---|---|---|")

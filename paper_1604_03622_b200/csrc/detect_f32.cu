@@ -74,8 +74,10 @@ __constant__ F32Plan c_f32;
 struct F32Args {
   int P, q, D, kb, G, mode, dft, ka;
   float scalef;  // dft: 1 / sqrt(P q); generic: 1 / sqrt(q)
-  float w4[F32_MAXG / 4][F32_MAXP][2];
 };
+// spatial-DFT candidate twiddles W_G^{g0 i} (dft grid): constant bank, so the
+// unrolled candidate loop reads them as immediate FFMA operands
+__constant__ float c_w4[F32_MAXG / 4][F32_MAXP][2];
 
 // In-place DFT of one pencil (R elements at base + r * st) in registers.
 // Pairs: X_u = A - iB, X_{R-u} = A + iB with s_r = t_r + t_{R-r},
@@ -85,10 +87,11 @@ struct F32Args {
 // wt[(u-1) h + (r-1)] = W_R^{u r mod R} = (cos, -sin) (warp-uniform
 // addresses: broadcast reads). ctw (Cooley-Tukey b-dim stages):
 // W_F^{r k1} = ctw[(r k1) mod F].
-template <int R>
-__device__ __forceinline__ void pencil(float2* __restrict__ a, int base, int st,
+template <int R, int ST = 0>  // ST > 0: compile-time element stride (fixed plans)
+__device__ __forceinline__ void pencil(float2* __restrict__ a, int base, int st_rt,
                                        const float2* __restrict__ wt,
                                        const float2* __restrict__ ctw, int twF, int k1) {
+  const int st = ST > 0 ? ST : st_rt;
   constexpr bool even = (R % 2) == 0;
   constexpr int h = pencil_h(R);
   float2 t[R];
@@ -174,6 +177,17 @@ __device__ __forceinline__ void stage_rows(float2* buf, int nr, int D, const F32
   }
 }
 
+// fixed-plan stage: R, stride and pencil count are compile-time constants, the
+// pencil bases ((pn / ST) R ST + pn % ST) are computed, no Cooley-Tukey factor
+template <int R, int ST, int NPEN>
+__device__ __forceinline__ void stage_fixed(float2* buf, int nr, int D, const float2* wt) {
+  for (int wi = threadIdx.x; wi < nr * NPEN; wi += F32_NT) {
+    const int row = (wi >= NPEN) + (wi >= 2 * NPEN), pn = wi - row * NPEN;
+    const int base = (pn / ST) * (R * ST) + pn % ST;
+    pencil<R, ST>(buf + (size_t)row * D, base, ST, wt, nullptr, 0, 0);
+  }
+}
+
 __device__ __forceinline__ void run_stage(float2* buf, int nr, int D, const F32Stage& s,
                                           const uint16_t* bases, const float2* wt,
                                           const float2* __restrict__ ctw) {
@@ -227,7 +241,7 @@ __device__ __forceinline__ float dft_cand(const float2 (&y)[F32_MAXP], int P, in
   t[0] = y[0];
 #pragma unroll
   for (int i = 1; i < 4; ++i) {
-    const float wx = fa.w4[g0][i][0], wy = fa.w4[g0][i][1];
+    const float wx = c_w4[g0][i][0], wy = c_w4[g0][i][1];
     t[i] = (i < P) ? make_float2(y[i].x * wx - y[i].y * wy, y[i].x * wy + y[i].y * wx)
                    : make_float2(0.0f, 0.0f);
   }
@@ -485,7 +499,9 @@ __global__ void f32_spec_kernel(const cplx* __restrict__ in, float2* __restrict_
 
 // Dynamic shared memory: two NR x D c64 row buffers | W tables (nw c64) |
 // pos_in, pos_out (D u16 each) | pencil bases (nbase u16).
-template <int NR>
+// PL = 0: any plan (stages from c_f32); PL = 1: D = 2001 = 3 x 23 x 29
+// (the Gotcha Doppler bank), every stage a compile-time instantiation
+template <int NR, int PL>
 __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
     const cplx* __restrict__ cube, int64_t n, const cplx* __restrict__ ub,
     const float2* __restrict__ ubf, const cplx* __restrict__ ua, const cplx* __restrict__ hconj,
@@ -537,9 +553,18 @@ __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
   int cur = 0;
   for (;; m += g, cur ^= 1) {
     if (fa.mode == 1) classical_coef<NR>(s_c, s_cf[cur], s_ua, P, fa.ka, kb);
-    for (int s = 0; s < c_f32.nst; ++s) {  // prime-factor DFT of bin m (FP32)
-      run_stage(bufs[cur], NR, D, c_f32.s[s], s_base, s_wt, ctw);
+    if (PL == 1) {  // prime-factor DFT of bin m (FP32), 2001 = 3 x 23 x 29
+      stage_fixed<3, 667, 667>(bufs[cur], NR, 2001, s_wt + c_f32.s[0].woff);
       __syncthreads();
+      stage_fixed<23, 29, 87>(bufs[cur], NR, 2001, s_wt + c_f32.s[1].woff);
+      __syncthreads();
+      stage_fixed<29, 1, 69>(bufs[cur], NR, 2001, s_wt + c_f32.s[2].woff);
+      __syncthreads();
+    } else {
+      for (int s = 0; s < c_f32.nst; ++s) {  // prime-factor DFT of bin m (FP32)
+        run_stage(bufs[cur], NR, D, c_f32.s[s], s_base, s_wt, ctw);
+        __syncthreads();
+      }
     }
     const int64_t mn = m + g;
     if (tid == 0 && mn + g < n) prefetch_bin(cube, mn + g, P, q);
@@ -775,13 +800,17 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
   fa.ka = (mode == 1 || spatial) ? ka : 0;
   fa.dft = dft ? 1 : 0;
   fa.scalef = (float)(dft ? 1.0 / sqrt((double)p * (double)q) : 1.0 / sqrt((double)q));
-  for (int g0 = 0; g0 < F32_MAXG / 4; ++g0)
-    for (int i = 0; i < F32_MAXP; ++i) {
-      const long double th = -2.0L * 3.141592653589793238462643383279502884L *
-                             (long double)((g0 * i) % G) / (long double)G;
-      fa.w4[g0][i][0] = (float)cosl(th);
-      fa.w4[g0][i][1] = (float)sinl(th);
-    }
+  {
+    float w4[F32_MAXG / 4][F32_MAXP][2];
+    for (int g0 = 0; g0 < F32_MAXG / 4; ++g0)
+      for (int i = 0; i < F32_MAXP; ++i) {
+        const long double th = -2.0L * 3.141592653589793238462643383279502884L *
+                               (long double)((g0 * i) % G) / (long double)G;
+        w4[g0][i][0] = (float)cosl(th);
+        w4[g0][i][1] = (float)sinl(th);
+      }
+    KST_TRY(const_upload(ctx, (const void*)&c_w4, w4, sizeof(w4), st));
+  }
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -789,22 +818,32 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)nsm * KST_F32_MINB);
-  switch (nr) {
-#define KST_F32_LAUNCH(NRR)                                                                      \
-  case NRR: {                                                                                    \
+  // the Gotcha Doppler bank has a compile-time plan (stage order 3, 23, 29)
+  static const bool fixed_on = !(getenv("KST_F32_FIXED") && atoi(getenv("KST_F32_FIXED")) == 0);
+  const F32Plan& pl = cp.plan;
+  const int PLv = (fixed_on && D == 2001 && pl.nst == 3 && pl.s[0].R == 3 && pl.s[0].st == 667 &&
+                   pl.s[1].R == 23 && pl.s[1].st == 29 && pl.s[2].R == 29 && pl.s[2].st == 1)
+                      ? 1
+                      : 0;
+  switch (nr * 2 + PLv) {
+#define KST_F32_LAUNCH(NRR, PLL)                                                                 \
+  case NRR * 2 + PLL: {                                                                          \
     static bool attr = false;                                                                    \
     if (!attr) {                                                                                 \
-      KST_CUDA(ctx, cudaFuncSetAttribute(detect_f32_kernel<NRR>,                                 \
+      KST_CUDA(ctx, cudaFuncSetAttribute(detect_f32_kernel<NRR, PLL>,                            \
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024)); \
       attr = true;                                                                               \
     }                                                                                            \
-    detect_f32_kernel<NRR><<<grid, F32_NT, smem, st>>>(cube, n, ub, ubf, ua ? ua : hconj, hconj, \
-                                                       u16_d, w_d, ctw_d, qh, qf, fa, values,    \
-                                                       flag);                                    \
+    detect_f32_kernel<NRR, PLL><<<grid, F32_NT, smem, st>>>(cube, n, ub, ubf, ua ? ua : hconj,   \
+                                                            hconj, u16_d, w_d, ctw_d, qh, qf, fa, \
+                                                            values, flag);                        \
   } break;
-    KST_F32_LAUNCH(1)
-    KST_F32_LAUNCH(2)
-    KST_F32_LAUNCH(3)
+    KST_F32_LAUNCH(1, 0)
+    KST_F32_LAUNCH(2, 0)
+    KST_F32_LAUNCH(3, 0)
+    KST_F32_LAUNCH(1, 1)
+    KST_F32_LAUNCH(2, 1)
+    KST_F32_LAUNCH(3, 1)
 #undef KST_F32_LAUNCH
   }
   KST_LAUNCH(ctx);

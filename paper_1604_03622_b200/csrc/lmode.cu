@@ -84,9 +84,20 @@ __host__ __device__ __forceinline__ int64_t win_start(int64_t m, int n_w, int64_
 // chunks of BG_TQ pulses (each bin row read once per CTA, not once per
 // pair); thread = (m, group of KT offsets), its P x P x KT accumulators in
 // registers.
+// P = 3: 2 offsets per thread (36 accumulator doubles) and 2 CTAs per SM:
+// the kernel is shared-memory-latency bound, so warps beat register reuse
+// (A/B at Gotcha scale: KT 4 / 1 CTA 2.01 ms, KT 2 / 2 CTAs 1.39 ms, KT 1 /
+// 3 CTAs 1.49 ms)
+#ifndef KST_BG_KT3
+#define KST_BG_KT3 2
+#endif
+#ifndef KST_BG_MINB
+#define KST_BG_MINB 2
+#endif
 template <int P>
 struct BG {
-  static constexpr int KT = P <= 2 ? 8 : P == 3 ? 4 : 2;
+  static constexpr int KT = P <= 2 ? 8 : P == 3 ? KST_BG_KT3 : 2;
+  static constexpr int MINB = P == 3 ? KST_BG_MINB : 1;
 };
 constexpr int BG_TQ = 16;
 constexpr int BG_LD = BG_TQ + 1;  // padded smem row (bank spread)
@@ -96,7 +107,7 @@ constexpr int BG_LD = BG_TQ + 1;  // padded smem row (bank spread)
 // band_reduce_kernel sums them in split order. nsplit and qs depend on q only
 // (never on the tile), so a tile's W equals the full frame's bitwise.
 template <int P>
-__global__ void __launch_bounds__(NT) band_gram_kernel(const cplx* __restrict__ X, int nb, int q,
+__global__ void __launch_bounds__(NT, BG<P>::MINB) band_gram_kernel(const cplx* __restrict__ X, int nb, int q,
                                                        int n_w, int tb, int qs, int64_t wstride,
                                                        cplx* __restrict__ W, cplx* __restrict__ rs) {
   constexpr int KT = BG<P>::KT;

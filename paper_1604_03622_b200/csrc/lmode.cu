@@ -925,68 +925,104 @@ struct DetArgs {
   double inv_sqrt_q;
 };
 
+// Thread = (test bin b, K quarter kq, Doppler dd): the three channel outputs
+// of bin b at Doppler dd over window rows [kq K4, (kq + 1) K4), three
+// independent FP64 chains sharing each X load (E rows broadcast within the
+// warp); the four K partials are summed in quarter order by the candidate
+// pass (deterministic). The X chunk of the next DT_TD Dopplers is staged by
+// cp.async into the second buffer while the current one is consumed (when
+// both fit the smem budget).
+constexpr int DT_KQ = 4;  // K split of the window rows
 template <int P>
 __global__ void __launch_bounds__(NT) lm_detect_kernel(const cplx* __restrict__ spec,
                                                        const cplx* __restrict__ Ein,
                                                        const cplx* __restrict__ hconj, DetArgs g,
-                                                       double* __restrict__ values) {
+                                                       int nbuf, double* __restrict__ values) {
   extern __shared__ __align__(16) cplx dsm[];
   const int n_w = g.n_w, nwp = n_w * P;
   cplx* Es = dsm;                    // DT_TB x P x nwp
-  cplx* Xs = Es + DT_TB * P * nwp;   // span x P x DT_LD
+  cplx* Xb = Es + DT_TB * P * nwp;   // nbuf x (span x P x DT_LD)
   __shared__ cplx Hs[64 * 4];
-  __shared__ cplx Ys[DT_TB * P * DT_TD];
+  __shared__ cplx Yp[DT_KQ * DT_TB * P * DT_TD];  // K-quarter partials
   const int64_t t0 = g.lo + (int64_t)blockIdx.x * DT_TB;
   const int nt = (int)min((int64_t)DT_TB, g.hi - t0);
   const int64_t sf = win_start(t0, n_w, g.n_bins);
   const int span = (int)(win_start(t0 + nt - 1, n_w, g.n_bins) + n_w - sf);
+  const size_t xsz = (size_t)span * P * DT_LD;
   for (int e = threadIdx.x; e < nt * P * nwp; e += NT)
     cp_async16(&Es[e], &Ein[(size_t)(t0 - g.lo) * P * nwp + e]);
   for (int e = threadIdx.x; e < g.G * P; e += NT) Hs[e] = hconj[e];
-  int off[DT_TB];
-#pragma unroll
-  for (int b = 0; b < DT_TB; ++b) off[b] = b < nt ? (int)(win_start(t0 + b, n_w, g.n_bins) - sf) : 0;
-  for (int d0 = 0; d0 < g.D; d0 += DT_TD) {
+  const int b = threadIdx.x / (DT_KQ * DT_TD), kq = (threadIdx.x / DT_TD) % DT_KQ,
+            dd = threadIdx.x % DT_TD;
+  const int kqn = (nwp + DT_KQ - 1) / DT_KQ, k0 = kq * kqn, k1 = min(nwp, k0 + kqn);
+  const int base = b < nt ? (int)(win_start(t0 + b, n_w, g.n_bins) - sf) * P : 0;
+  auto stage = [&](int d0, cplx* Xs) {
     const int dl = min(DT_TD, g.D - d0);
-    __syncthreads();  // previous chunk consumed
     for (int e = threadIdx.x; e < span * P * DT_TD; e += NT) {
       const int row = e / DT_TD, c = e - row * DT_TD;
       if (c < dl)
         cp_async16(&Xs[row * DT_LD + c], &spec[((sf - g.a) * P + row) * (int64_t)g.D + d0 + c]);
     }
     cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    for (int o = threadIdx.x; o < nt * P * DT_TD; o += NT) {
-      const int b = o / (P * DT_TD), i = (o / DT_TD) % P, dd = o % DT_TD;
-      const cplx* er = Es + (b * P + i) * nwp;
-      const cplx* xr = Xs + dd;
-      int base = 0;
-#pragma unroll
-      for (int bb = 0; bb < DT_TB; ++bb)
-        if (bb == b) base = off[bb] * P;
-      cplx acc = cmk(0, 0);
-      if (dd < dl)
-        for (int jx = 0; jx < nwp; ++jx) cfma(acc, er[jx], xr[(base + jx) * DT_LD]);
-      Ys[o] = acc;
+  };
+  stage(0, Xb);
+  int buf = 0;
+  for (int d0 = 0; d0 < g.D; d0 += DT_TD) {
+    const int dl = min(DT_TD, g.D - d0);
+    const bool next = d0 + DT_TD < g.D;
+    if (nbuf == 2 && next) {
+      stage(d0 + DT_TD, Xb + (size_t)(buf ^ 1) * xsz);  // its slot was freed by the last barrier
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
-    __syncthreads();
+    __syncthreads();  // chunk d0 (and E) visible
+    const cplx* Xs = Xb + (size_t)buf * xsz;
+    if (b < nt && dd < dl) {
+      cplx acc[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) acc[i] = cmk(0, 0);
+      const cplx* er = Es + (size_t)b * P * nwp;
+      const cplx* xr = Xs + (size_t)base * DT_LD + dd;
+#pragma unroll 4
+      for (int jx = k0; jx < k1; ++jx) {
+        const cplx x = xr[jx * DT_LD];
+#pragma unroll
+        for (int i = 0; i < P; ++i) cfma(acc[i], er[i * nwp + jx], x);
+      }
+#pragma unroll
+      for (int i = 0; i < P; ++i) Yp[((kq * DT_TB + b) * P + i) * DT_TD + dd] = acc[i];
+    }
+    __syncthreads();  // partials ready; chunk d0's X slot may be refilled
     for (int o = threadIdx.x; o < nt * DT_TD; o += NT) {
-      const int b = o / DT_TD, dd = o % DT_TD;
-      if (dd >= dl) continue;
+      const int bb = o / DT_TD, d2 = o % DT_TD;
+      if (d2 >= dl) continue;
+      cplx y[P];
+#pragma unroll
+      for (int i = 0; i < P; ++i) {
+        cplx v = Yp[((0 * DT_TB + bb) * P + i) * DT_TD + d2];
+#pragma unroll
+        for (int k = 1; k < DT_KQ; ++k) v = cadd(v, Yp[((k * DT_TB + bb) * P + i) * DT_TD + d2]);
+        y[i] = v;
+      }
       double best2 = -1.0;
       cplx zb = cmk(0, 0);
       for (int gg = 0; gg < g.G; ++gg) {
         cplx z = cmk(0, 0);
 #pragma unroll
-        for (int i = 0; i < P; ++i) cfma(z, Hs[gg * P + i], Ys[(b * P + i) * DT_TD + dd]);
+        for (int i = 0; i < P; ++i) cfma(z, Hs[gg * P + i], y[i]);
         const double m2 = cabs2(z);
         if (m2 > best2) {
           best2 = m2;
           zb = z;
         }
       }
-      values[(t0 + b - g.lo) * (int64_t)g.D + d0 + dd] = hypot(zb.x * g.inv_sqrt_q, zb.y * g.inv_sqrt_q);
+      values[(t0 + bb - g.lo) * (int64_t)g.D + d0 + d2] = hypot(zb.x * g.inv_sqrt_q, zb.y * g.inv_sqrt_q);
+    }
+    if (nbuf == 2) buf ^= 1;
+    else if (next) {
+      __syncthreads();  // single buffer: every read of chunk d0 done before restaging
+      stage(d0 + DT_TD, Xb);
     }
   }
 }
@@ -1048,10 +1084,10 @@ int launch_win(kst_ctx* ctx, const cplx* W, const cplx* rs, const double* Qp, co
 
 template <int P>
 int launch_det(kst_ctx* ctx, const cplx* spec, const cplx* E, const cplx* hconj, const DetArgs& da,
-               double* values, int64_t n_test, size_t dsm, cudaStream_t st) {
+               double* values, int64_t n_test, size_t dsm, int nbuf, cudaStream_t st) {
   KST_CUDA(ctx, cudaFuncSetAttribute(lm_detect_kernel<P>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-  lm_detect_kernel<P><<<cdiv(n_test, DT_TB), NT, dsm, st>>>(spec, E, hconj, da, values);
+  lm_detect_kernel<P><<<cdiv(n_test, DT_TB), NT, dsm, st>>>(spec, E, hconj, da, nbuf, values);
   KST_LAUNCH(ctx);
   return KST_OK;
 }
@@ -1199,11 +1235,15 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   da.D = D;
   da.G = G;
   da.inv_sqrt_q = 1.0 / sqrt((double)q);
-  const size_t dsm = sizeof(cplx) * ((size_t)DT_TB * p * nwp + (size_t)(DT_TB + n_w - 1) * p * DT_LD);
+  // E rows + one or two X chunks (double-buffered when both fit 200 KB)
+  const size_t xchunk = sizeof(cplx) * (size_t)(DT_TB + n_w - 1) * p * DT_LD;
+  const size_t ebytes = sizeof(cplx) * (size_t)DT_TB * p * nwp;
+  const int nbuf = ebytes + 2 * xchunk <= 200 * 1024 ? 2 : 1;
+  const size_t dsm = ebytes + nbuf * xchunk;
   switch (p) {
-    case 1: KST_TRY(launch_det<1>(ctx, spec, E, hconj, da, values, n_test, dsm, st)); break;
-    case 2: KST_TRY(launch_det<2>(ctx, spec, E, hconj, da, values, n_test, dsm, st)); break;
-    default: KST_TRY(launch_det<3>(ctx, spec, E, hconj, da, values, n_test, dsm, st)); break;
+    case 1: KST_TRY(launch_det<1>(ctx, spec, E, hconj, da, values, n_test, dsm, nbuf, st)); break;
+    case 2: KST_TRY(launch_det<2>(ctx, spec, E, hconj, da, values, n_test, dsm, nbuf, st)); break;
+    default: KST_TRY(launch_det<3>(ctx, spec, E, hconj, da, values, n_test, dsm, nbuf, st)); break;
   }
   KST_LAUNCH(ctx);
   // 5. window statuses: errors raise in window order (the reference's loop

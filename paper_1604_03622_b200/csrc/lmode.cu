@@ -440,8 +440,11 @@ __device__ __forceinline__ void rotate_block(cplx* Y, int nb, int s, const JacSm
 // info per window (ints): status, iterations, converged, ka, kb, eig rounds, r, nb
 constexpr int WI = 8;
 
+#ifndef KST_WIN_MINB
+#define KST_WIN_MINB 2
+#endif
 template <int P>
-__global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ W,
+__global__ void __launch_bounds__(NT, KST_WIN_MINB) window_kernel(const cplx* __restrict__ W,
                                                        const cplx* __restrict__ rs,
                                                        const double* __restrict__ Qp, WinArgs g,
                                                        cplx* __restrict__ Hscr,
@@ -463,6 +466,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
   cplx* cmall = gam + (size_t)g.n_w * P * LM_KBMAX;  // (n_w / 2 + 1) x P x LM_KBMAX
   __shared__ double red[4 + 2 * U + 2 * E];
   __shared__ double recv[NREC + 1];
+  __shared__ double a0s[2 * U];
   __shared__ IterState st;
   __shared__ cplx spatial[kMaxP * kMaxP];
   __shared__ double dinfo[4], hdiag[8];
@@ -484,16 +488,38 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
     // ---------------------------------------------------------- (1) record
     // the window's pairs (m, m'), m <= m' in [s, s + n_w): for each of its
     // bins m = s + ml the offsets o < n_w - ml, i.e. the band-prefix entry
-    // Qp[m][slot][n_w - ml - 1] (band_prefix_kernel); thread = record slot,
-    // the n_w entries summed in bin order (deterministic, tile-independent)
+    // Qp[m][slot][n_w - ml - 1] (band_prefix_kernel); warp = record slot,
+    // lanes over the bins, fixed warp_sum tree (deterministic, tile-independent)
     {
       constexpr int NQ = 2 + 2 * E;
-      for (int k = tid; k < NQ; k += NT) {
-        double x = 0.0;
-#pragma unroll 8
-        for (int ml = 0; ml < n_w; ++ml)
-          x += Qp[((int64_t)(s + ml) * NQ + k) * n_w + (n_w - 1 - ml)];
-        recv[k] = x;
+      const int wid = tid >> 5, lane = tid & 31;
+      // warp per 4 slots (12 independent loads in flight per lane), lanes over the bins
+      for (int k0 = 4 * wid; k0 < NQ; k0 += 4 * (NT / 32)) {
+        double x[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int ml = lane; ml < n_w; ml += 32) {
+          const double* qb = Qp + (int64_t)(s + ml) * NQ * n_w + (n_w - 1 - ml);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (k0 + c < NQ) x[c] += qb[(int64_t)(k0 + c) * n_w];
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double t = warp_sum(x[c]);
+          if (lane == 0 && k0 + c < NQ) recv[k0 + c] = t;
+        }
+      }
+      // A0 block sums (1/n) sum_m s_m[i] conj(s_m[j]): warp per block entry
+      for (int u = wid; u < U; u += NT / 32) {
+        const int i = u / P, j = u % P;
+        cplx acc = cmk(0, 0);
+        for (int ml = lane; ml < n_w; ml += 32)
+          cfmac(acc, rs[(int64_t)(s + ml) * P + i], rs[(int64_t)(s + ml) * P + j]);
+        acc.x = warp_sum(acc.x);
+        acc.y = warp_sum(acc.y);
+        if (lane == 0) {
+          a0s[2 * u] = acc.x;
+          a0s[2 * u + 1] = acc.y;
+        }
       }
       __syncthreads();
       const double inv_n2 = 1.0 / (nn * nn);
@@ -504,12 +530,7 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
         else if (k == 2) x = 0.0;  // window S diagonal = (1/n) sum |x|^2 >= 0
         else if (k == 3) x = 1.0;
         else if (k < 4 + 2 * U) {
-          // A0 block sums: (1/n) sum_m s_m[i] conj(s_m[j])  (re at even, im at odd)
-          const int u = (k - 4) >> 1, i = u / P, j = u % P;
-          cplx acc = cmk(0, 0);
-          for (int ml = 0; ml < n_w; ++ml)
-            cfmac(acc, rs[(int64_t)(s + ml) * P + i], rs[(int64_t)(s + ml) * P + j]);
-          x = ((k - 4) & 1 ? acc.y : acc.x) / nn;
+          x = a0s[k - 4] / nn;  // A0 block sums (re at even, im at odd)
         } else {
           x = recv[2 + (k - 4 - 2 * U)] * inv_n2;
         }
@@ -607,19 +628,34 @@ __global__ void __launch_bounds__(NT, 2) window_kernel(const cplx* __restrict__ 
     const int kk = zero_s ? 0 : min(g.rb, nb);
     cplx* H = Hscr + (size_t)blockIdx.x * g.nbmax * g.nbmax;
     if (!zero_s) {
-      for (int e = tid; e < nb * nb; e += NT) {
-        const int row = e / nb, col = e - row * nb;
-        const int m1 = row / r, k1 = row - m1 * r, m2 = col / r, k2 = col - m2 * r;
-        // a_k1^H W_{m1 m2} a_k2
-        cplx acc = cmk(0, 0);
+      // upper block pairs (m1 = ml, m2 = ml + o) of the band, each W block read
+      // once: H[(m1,k1),(m2,k2)] = sqrt(om_k1 om_k2) a_k1^H W_{m1 m2} a_k2 and the
+      // mirror H[(m2,k2),(m1,k1)] = conj (H Hermitian by construction)
+      for (int e = tid; e < n_w * n_w; e += NT) {
+        const int ml = e / n_w, o = e - ml * n_w;
+        if (o >= n_w - ml) continue;
+        const cplx* bp = W + ((int64_t)(s + ml) * n_w + o) * NPW;
+        cplx B[NPW];
 #pragma unroll
-        for (int i = 0; i < P; ++i) {
-          cplx wa = cmk(0, 0);
+        for (int k = 0; k < NPW; ++k) B[k] = bp[k];
+        for (int k2 = 0; k2 < r; ++k2) {
+          cplx wa[P];
 #pragma unroll
-          for (int jj = 0; jj < P; ++jj) cfma(wa, wget<P>(W, n_w, s + m1, s + m2, i, jj), av[jj * P + k2]);
-          cfmca(acc, av[i * P + k1], wa);
+          for (int i = 0; i < P; ++i) {
+            wa[i] = cmk(0, 0);
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) cfma(wa[i], B[i * P + jj], av[jj * P + k2]);
+          }
+          for (int k1 = 0; k1 < r; ++k1) {
+            cplx acc = cmk(0, 0);
+#pragma unroll
+            for (int i = 0; i < P; ++i) cfmca(acc, av[i * P + k1], wa[i]);
+            const cplx h = cscale(acc, sqrt(omega[k1] * omega[k2]));
+            const int row = ml * r + k1, col = (ml + o) * r + k2;
+            H[(int64_t)row * nb + col] = h;
+            if (o) H[(int64_t)col * nb + row] = cconj(h);
+          }
         }
-        H[e] = cscale(acc, sqrt(omega[k1] * omega[k2]));
       }
       __syncthreads();
       LM_STAMP(w, 4);
@@ -1147,7 +1183,7 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const int nslot = std::min(nwin, 2 * nsm);
+  const int nslot = std::min(nwin, KST_WIN_MINB * nsm);
   // n_w r, r = rank of the b-producing spatial iterate: r_a, or p when the
   // loop stops after its first iteration (A_prev = A0)
   const int nbmax = std::min(LM_NBMAX, n_w * (max_iter == 1 ? p : rank_spatial));

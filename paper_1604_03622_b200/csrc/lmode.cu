@@ -64,8 +64,12 @@ __device__ long long lm_prof[4096][16];
 #endif
 
 constexpr int LM_NWMAX = 128;  // training window of the batched path
-constexpr int LM_KBMAX = 6;    // temporal basis width of the batched path
-constexpr int LM_S = 8;        // subspace block
+constexpr int LM_KBMAX = 3;    // temporal basis width of the batched path (r_b <= LM_S - 2)
+// subspace block: the r_b <= 3 wanted pairs + 2 guard vectors (A/B on
+// configs[3]: s = 5 converges in the same 2 rounds as s = 8 with eig(H) 173 ->
+// 96 us per window; CGS and the Rayleigh-Ritz Jacobi scale with s^2). Larger
+// r_b run on the per-window step path.
+constexpr int LM_S = 5;
 constexpr int LM_JAC = 16;     // n_w r <= this: dense Jacobi instead of subspace iteration
 constexpr int LM_NBMAX = 256;  // n_w r limit (block vectors in smem)
 constexpr int LM_MAXR = 24;    // Rayleigh-Ritz rounds before falling back
@@ -358,47 +362,62 @@ __device__ __forceinline__ void block_gram(const cplx* A, const cplx* B, int nb,
 }
 
 // Orthonormalise the nb x s block Y in place by classical Gram-Schmidt with
-// reorthogonalisation (CGS2), column by column: stable for the very
-// ill-conditioned blocks a dominant mover produces after one H step (where
+// selective reorthogonalisation (a second pass when the first cancelled more
+// than half of the norm -- "twice is enough"), column by column: stable for
+// the very ill-conditioned blocks a dominant mover produces after one H step (where
 // Cholesky-QR, which squares the condition number, breaks down). A column
 // that vanishes after projection (relative 1e-13) is replaced by the next
 // unused unit vector and re-projected. Warp j forms coefficient j (lanes
 // stride the rows, fixed shuffle tree: deterministic).
 __device__ void cgs2(cplx* Y, int nb, int s, cplx* coef, double* nrm, int* next_unit) {
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // y_k -= sum_{j<k} <y_j, y_k> y_j: warps j < k form the coefficients (warp
+  // NT/32 - 1 meanwhile |y_k|^2 into nrm[0] when want_n0), then every row
+  // updates; ends with |y_k|^2 in nrm[1] visible to all
+  auto project = [&](int k, bool want_n0) {
+    if (wid < k) {
+      cplx acc = cmk(0, 0);
+      for (int r = lane; r < nb; r += 32) cfmca(acc, Y[r * LM_S + wid], Y[r * LM_S + k]);
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      if (lane == 0) coef[wid] = acc;
+    } else if (want_n0 && wid == NT / 32 - 1) {
+      double a = 0.0;
+      for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
+      a = warp_sum(a);
+      if (lane == 0) nrm[0] = a;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < nb; r += NT) {
+      cplx y = Y[r * LM_S + k];
+      for (int j2 = 0; j2 < k; ++j2) y = csub(y, cmul(Y[r * LM_S + j2], coef[j2]));
+      Y[r * LM_S + k] = y;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double a = 0.0;
+      for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
+      a = warp_sum(a);
+      if (lane == 0) nrm[1] = a;
+    }
+    __syncthreads();
+  };
   for (int k = 0; k < s; ++k) {
     for (int attempt = 0; attempt < 2; ++attempt) {
-      // |y_k|^2 before projection
-      if (wid == 0) {
-        double a = 0.0;
-        for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
-        a = warp_sum(a);
-        if (lane == 0) nrm[0] = a;
-      }
-      for (int pass = 0; pass < 2 && k > 0; ++pass) {
-        __syncthreads();
-        if (wid < k) {
-          cplx acc = cmk(0, 0);
-          for (int r = lane; r < nb; r += 32) cfmca(acc, Y[r * LM_S + wid], Y[r * LM_S + k]);
-          acc.x = warp_sum(acc.x);
-          acc.y = warp_sum(acc.y);
-          if (lane == 0) coef[wid] = acc;
+      if (k == 0) {
+        if (wid == 0) {
+          double a = 0.0;
+          for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
+          a = warp_sum(a);
+          if (lane == 0) nrm[0] = nrm[1] = a;
         }
         __syncthreads();
-        for (int r = threadIdx.x; r < nb; r += NT) {
-          cplx y = Y[r * LM_S + k];
-          for (int j2 = 0; j2 < k; ++j2) y = csub(y, cmul(Y[r * LM_S + j2], coef[j2]));
-          Y[r * LM_S + k] = y;
-        }
+      } else {
+        project(k, true);
+        // "twice is enough" (Kahan-Parlett): reorthogonalise only when the
+        // projection cancelled more than half of the norm
+        if (nrm[1] <= 0.25 * nrm[0]) project(k, false);  // nrm[0] keeps |y_k|^2 before
       }
-      __syncthreads();
-      if (wid == 0) {
-        double a = 0.0;
-        for (int r = lane; r < nb; r += 32) a += cabs2(Y[r * LM_S + k]);
-        a = warp_sum(a);
-        if (lane == 0) nrm[1] = a;
-      }
-      __syncthreads();
       const bool ok = nrm[1] > 1e-26 * nrm[0] && nrm[1] > 0.0;
       if (ok || attempt == 1) break;
       // dependent column: restart it as the next unit vector
@@ -1163,7 +1182,7 @@ extern "C" int kst_lmode(kst_ctx* ctx, const double* cube, int64_t a, int64_t n_
   if (a > s_lo) return set_err(ctx, KST_ERR_DIMENSION, "lmode: tile cube starts after its halo");
   const int nwin = (int)(s_hi - s_lo + 1);
   static const bool batched_env = !(getenv("KST_LMODE") && strcmp(getenv("KST_LMODE"), "serial") == 0);
-  const bool supported = batched_env && p <= 3 && n_w <= LM_NWMAX && rank_temporal <= LM_KBMAX &&
+  const bool supported = batched_env && p <= 3 && n_w <= LM_NWMAX && rank_temporal <= LM_S - 2 &&
                          rank_temporal < q && G <= 64 &&
                          (kind == KST_KIND_KRON || kind == KST_KIND_CLASSICAL);
   if (!supported) {

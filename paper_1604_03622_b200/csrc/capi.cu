@@ -76,6 +76,74 @@ void* pinned_get(kst_ctx* ctx, size_t bytes) {
   return ctx->pinned;
 }
 
+// ---------------------------------------------------------------- optimistic pipeline
+// Device forms of the host decisions of kst_pipeline's common case, so a frame
+// runs without a stream synchronisation until its end:
+//
+// spatial_basis_kernel: subspace_basis(spatial, r_a) (src/filters.py:58-73)
+//   from the Jacobi pairs of the P x P spatial factor: the Hermitian check of
+//   herm_check, the kept count k (values > 1e-9 of the top one, <= r), and
+//   the first r eigenvectors copied with pitch r (the caller assumed k = r).
+__global__ void spatial_basis_kernel(const cplx* __restrict__ M, int p, const double* __restrict__ vals,
+                                     const cplx* __restrict__ vecs, int r, cplx* __restrict__ ua,
+                                     int* __restrict__ flags) {
+  if (threadIdx.x == 0) {
+    double f = 0.0, a = 0.0;
+    int bad = 0;
+    for (int i = 0; i < p; ++i)
+      for (int j = 0; j < p; ++j) {
+        const cplx x = M[i * p + j], y = M[j * p + i];
+        if (!isfinite(x.x) || !isfinite(x.y)) bad = 1;
+        f += cabs2(x);
+        a += cabs2(cmk(x.x - y.x, x.y + y.y));
+      }
+    const double scale = sqrt(f);
+    flags[0] = (!bad && !(scale > 0 && sqrt(a) > 1e-8 * scale)) ? 1 : 0;  // Hermitian
+    int k = 0;
+    const double top = vals[0];
+    if (top > 0.0)
+      while (k < r && vals[k] > 1e-9 * top) ++k;
+    flags[1] = k;
+  }
+  for (int e = threadIdx.x; e < p * r; e += blockDim.x) {
+    const int i = e / r, c = e % r;
+    ua[e] = vecs[i * p + c];
+  }
+}
+
+// pipeline_check_kernel: the kept temporal rank from the top-r_b values of b
+// (capi: clamp of src/linalg.py:138-140, keep rule src/filters.py:70) and the
+// validation of every assumption of the optimistic schedule; rec =
+// {ok, iterations, converged, ka, kb, last residual}.
+__global__ void pipeline_check_kernel(const double* __restrict__ tbv, int rb, const double* __restrict__ dres,
+                                      int max_iter, const double* __restrict__ diag,
+                                      const int* __restrict__ heig_ok, const int* __restrict__ flags,
+                                      int ka_assumed, double* __restrict__ rec) {
+  if (threadIdx.x != 0) return;
+  double top = 0.0;
+  for (int k = 0; k < rb; ++k) top = fmax(top, fabs(tbv[k]));
+  double v0 = tbv[0];
+  if (v0 < 0 && fabs(v0) <= 1e-10 * top) v0 = 0.0;
+  int kb = 0;
+  if (v0 > 0.0)
+    while (kb < rb) {
+      double v = tbv[kb];
+      if (v < 0 && fabs(v) <= 1e-10 * top) v = 0.0;
+      if (!(v > 1e-9 * v0)) break;
+      ++kb;
+    }
+  const int status = (int)dres[max_iter], iters = (int)dres[max_iter + 1],
+            conv = (int)dres[max_iter + 2];
+  const bool ok = status == 0 && diag[0] == 0.0 && diag[3] > 0.0 && iters >= 1 && *heig_ok == 1 &&
+                  flags[0] == 1 && flags[1] == ka_assumed && kb == rb;
+  rec[0] = ok ? 1.0 : 0.0;
+  rec[1] = iters;
+  rec[2] = conv;
+  rec[3] = flags[1];
+  rec[4] = kb;
+  rec[5] = iters >= 1 ? dres[iters - 1] : 0.0;
+}
+
 extern "C" {
 
 int kst_version(void) { return 1; }
@@ -267,6 +335,61 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   stage_mark(ctx, 1, st);
   // the temporal basis must survive until detection: dedicated slot
   const bool full_b = rank_temporal == q;
+  // Optimistic host-sync-free form of the common case (p <= 4, q > 64,
+  // r_b <= 24): estimator, bases and detection are enqueued back to back
+  // with every decision (convergence, kept ranks, validity) taken on the
+  // device; ONE synchronisation at the end reads the outcome. When any
+  // assumption fails (non-finite or zero S, a degenerate iterate, the
+  // eigensolver needing more than one round, k_A < r_A, k_B < r_B) the
+  // frame is recomputed from S by the synchronous path below, so results
+  // equal the synchronous path's either way.
+  static const bool async_env = !(getenv("KST_PIPE_ASYNC") && atoi(getenv("KST_PIPE_ASYNC")) == 0);
+  if (async_env && !full_b && p <= 4 && q > 64 /* heig_top Jacobi limit */ && rank_spatial >= 1 &&
+      rank_spatial <= p && rank_temporal >= 1 && rank_temporal <= 24 && max_iter >= 1) {
+    cplx* ubA = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);
+    // spatial (p^2) | ua (p^2) | Jacobi vectors (p^2) | values (p) | rec (8) | flags
+    char* sp = (char*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 3 + sizeof(double) * (p + 8) + 64);
+    double* hrec = (double*)pinned_get(ctx, 256);
+    if (!ubA || !sp || !hrec) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+    cplx* spA = (cplx*)sp;
+    cplx* uaA = spA + p * p;
+    cplx* vecA = uaA + p * p;
+    double* valA = (double*)(vecA + p * p);
+    double* rec = valA + p;
+    int* flags = (int*)(rec + 8);
+    int* heig_ok = flags + 2;
+    const double* tbv_dev = nullptr;
+    const double* dres = nullptr;
+    const double* diag = nullptr;
+    KST_TRY(kst::lrkron_async(ctx, S, p, q, rank_spatial, rank_temporal, tol, max_iter, spA, ubA,
+                              heig_ok, &tbv_dev, &dres, &diag, st));
+    stage_mark(ctx, 2, st);
+    KST_TRY(kst::small_heig(ctx, spA, p, valA, vecA, st));
+    const int ka = rank_spatial;
+    spatial_basis_kernel<<<1, 32, 0, st>>>(spA, p, valA, vecA, ka, uaA, flags);
+    KST_LAUNCH(ctx);
+    stage_mark(ctx, 3, st);
+    KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, uaA, ka, ubA, rank_temporal, kind, 0,
+                        dopplers, D, (const cplx*)grid, G, groups, values, st, false));
+    stage_mark(ctx, 4, st);
+    pipeline_check_kernel<<<1, 32, 0, st>>>(tbv_dev, rank_temporal, dres, max_iter, diag, heig_ok,
+                                            flags, ka, rec);
+    KST_LAUNCH(ctx);
+    KST_CUDA(ctx, cudaMemcpyAsync(hrec, rec, sizeof(double) * 6, cudaMemcpyDeviceToHost, st));
+    KST_CUDA(ctx, cudaStreamSynchronize(st));
+    if (hrec[0] == 1.0) {
+      if (summary) {
+        summary[0] = hrec[1];
+        summary[1] = hrec[2];
+        summary[2] = hrec[3];
+        summary[3] = hrec[4];
+        summary[4] = hrec[5];
+        summary[5] = summary[6] = summary[7] = 0.0;
+      }
+      return KST_OK;
+    }
+    // an assumption failed: the synchronous path recomputes from S
+  }
   // ub: the top-rb eigenvectors (q x rb), then the kept kb columns repacked (q x kb)
   cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);
   cplx* temporal = full_b ? (cplx*)ws_get(ctx, WS_PIPE_T, sizeof(cplx) * (size_t)q * q) : nullptr;

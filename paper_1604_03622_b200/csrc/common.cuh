@@ -286,7 +286,7 @@ struct TopEig {
   cplx* vectors = nullptr;     // dev (n, r) row-major
 };
 int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cplx* vectors,
-             cudaStream_t st);
+             cudaStream_t st, int* ok_dev = nullptr, const double** values_dev_out = nullptr);
 int small_heig(kst_ctx* ctx, const cplx* M, int n, double* values_dev, cplx* vectors_dev,
                cudaStream_t st);
 int truncate_from_pairs(kst_ctx* ctx, const double* values_host, const cplx* vectors, int n,
@@ -303,6 +303,9 @@ struct FitOut {
 int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol, int max_iter,
            int validate, cplx* spatial, cplx* temporal, cplx* tb_vectors, double* tb_values,
            FitOut* fit, cplx* iter_spatial, cplx* iter_b, cudaStream_t st);
+int lrkron_async(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol, int max_iter,
+                 cplx* spatial, cplx* tb_vectors, int* heig_ok, const double** tb_vals_dev,
+                 const double** dres_out, const double** diag_out, cudaStream_t st);
 // detect.cu
 int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
            const cplx* ub, int kb, int kind, int spatial_only, const double* dop_host, int D,

@@ -342,6 +342,28 @@ __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict
   if (threadIdx.x < s) Z[(size_t)picked[threadIdx.x] * s + threadIdx.x] = cmk(1.0, 0.0);
 }
 
+// Device form of heig_top's round-0 convergence test (host loop below): every
+// wanted Ritz pair with residual <= 1e-12 max|theta|, or <= 1e-9 max|theta|
+// and <= 1e-8 of its gap; kept > 0. Same sums in the same order as the host.
+__global__ void rr_check_kernel(const double* __restrict__ res_part, int nup, int r,
+                                const double* __restrict__ th, int s, const int* __restrict__ info,
+                                int* __restrict__ ok) {
+  if (threadIdx.x != 0) return;
+  double tmax = 0.0;
+  for (int k = 0; k < s; ++k) tmax = fmax(tmax, fabs(th[k]));
+  bool all_ok = true;
+  for (int k = 0; k < r; ++k) {
+    double acc = 0.0;
+    for (int b = 0; b < nup; ++b) acc += res_part[(size_t)b * r + k];
+    const double res = sqrt(acc);
+    double gap = 1e300;
+    for (int jx = 0; jx < s; ++jx)
+      if (jx != k) gap = fmin(gap, fabs(th[k] - th[jx]));
+    all_ok = all_ok && (res <= 1e-12 * tmax || (res <= 1e-9 * tmax && res <= 1e-8 * gap));
+  }
+  *ok = (info[0] != 0 && (tmax == 0.0 || all_ok)) ? 1 : 0;
+}
+
 // Final ordering (descending, reference tie rule) + pivot phase for the top r
 // Ritz vectors; single CTA of 1024 threads, s <= 32. The pivot search (argmax
 // |Z[i][k]| per column, lowest index on ties) maps thread t to column t % s and
@@ -954,9 +976,16 @@ static int heig_top_cusolver(kst_ctx* ctx, const cplx* M, int n, int r, double* 
   return KST_OK;
 }
 
+// ok_dev != nullptr (host-sync-free form, n > kMaxN, r <= 24): the fixed
+// schedule of the common case -- warm-up, ONE Rayleigh-Ritz round -- with the
+// round-0 convergence test on the device (rr_check_kernel: 1 in *ok_dev when
+// the host loop would have stopped after that round, 0 otherwise), values
+// left on the device (*values_dev_out); no stream synchronisation.
 int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cplx* vectors,
-             cudaStream_t st) {
+             cudaStream_t st, int* ok_dev, const double** values_dev_out) {
   if (r < 1 || r > n) return set_err(ctx, KST_ERR_DIMENSION, "heig_top: r=%d n=%d", r, n);
+  if (ok_dev && (n <= kMaxN || r > 24))
+    return set_err(ctx, KST_ERR_DIMENSION, "heig_top: no sync-free form for n=%d r=%d", n, r);
   if (n <= kMaxN) {
     cplx* vec = (cplx*)ws_get(ctx, WS_EIG2, sizeof(cplx) * n * n + sizeof(double) * n);
     if (!vec) return set_err(ctx, KST_ERR_CUDA, "heig_top: workspace");
@@ -1038,6 +1067,18 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   KST_TRY(step(Z, Z, Y2, 1));
   KST_TRY(step(Z, Z, Z, 1));
 
+  if (ok_dev) {
+    KST_TRY(bz(ctx, M, n, Z, s, Y, st));
+    KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
+    cplx* Zcur = Z;
+    KST_TRY(step(Zcur, Y, Y2, 0));
+    rr_check_kernel<<<1, 32, 0, st>>>(res_part, nup, r, theta, s, info, ok_dev);
+    KST_LAUNCH(ctx);
+    finalize_top_kernel<<<1, 1024, 0, st>>>(X, n, s, r, theta, vout, vectors);
+    KST_LAUNCH(ctx);
+    if (values_dev_out) *values_dev_out = vout;
+    return KST_OK;
+  }
   bool converged = false;
   double prev_worst = 1e300;
   int stall = 0;

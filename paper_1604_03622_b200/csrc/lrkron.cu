@@ -900,4 +900,81 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   return KST_OK;
 }
 
+// Host-sync-free form of lrkron's M-path (p <= 4, rb < q, q > 64), for the
+// optimistic kst_pipeline: the same kernels -- mgram, m_iterate (every
+// iteration on the device), the final b-step, the top-rb eigenpairs of b by
+// heig_top's fixed common-case schedule -- with every outcome left on the
+// device: *dres_out = residuals[max_iter] then {status, iterations,
+// converged}; *diag_out = {bad, dmin, dmax, fro, na2_0}; *heig_ok = 1 when
+// the eigensolver converged in its first round. The caller validates these
+// on the device and re-runs the synchronous path when any check fails.
+int lrkron_async(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol, int max_iter,
+                 cplx* spatial, cplx* tb_vectors, int* heig_ok, const double** tb_vals_dev,
+                 const double** dres_out, const double** diag_out, cudaStream_t st) {
+  if (p < 1 || p > 4 || q <= kMaxN || ra < 1 || ra > p || rb < 1 || rb >= q || rb > 24 ||
+      max_iter < 1)
+    return set_err(ctx, KST_ERR_DIMENSION, "lrkron_async: unsupported shape");
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int rows_per = p == 3 ? (q + nsm - 1) / nsm : MG_ROWS;
+  const int nblk = (q + rows_per - 1) / rows_per;
+  const int nvx = (q + V_ROWS - 1) / V_ROWS, nbb = (q + NT - 1) / NT, nbx = (q + ST_ROWS - 1) / ST_ROWS;
+  size_t rec = 0;
+  KST_DISPATCH_P(p, (rec = MDims<PP>::STRIDE));
+  // the same slots and sizes as lrkron (WS_PART taken once for every use)
+  size_t part_bytes = std::max(sizeof(double) * STAT_STRIDE * p * nbx,
+                               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64);
+  part_bytes = std::max(part_bytes, sizeof(double) * rec * nblk + 64);
+  char* small = (char*)ws_get(ctx, WS_SMALL, sizeof(IterState) + 256);
+  double* part = (double*)ws_get(ctx, WS_PART, part_bytes);
+  cplx* b = (cplx*)ws_get(ctx, WS_B, sizeof(cplx) * (size_t)q * q);
+  double* dres = (double*)ws_get(ctx, WS_VALS, sizeof(double) * (max_iter + 8));
+  if (!small || !part || !b || !dres) return set_err(ctx, KST_ERR_CUDA, "lrkron_async: workspace");
+  IterState* state = (IterState*)small;
+  double* minfo = dres + max_iter;
+  double* diag = (double*)(small + sizeof(IterState));
+  const size_t jsm = jac_smem_bytes(p);
+  switch (p) {
+    case 1:
+      mgram_reg_kernel<1><<<nblk, NT, 0, st>>>(S, q, part);
+      m_iterate_kernel<1><<<1, NT, jsm, st>>>(part, nblk, q, ra, tol, max_iter, state, spatial,
+                                               dres, minfo, diag);
+      break;
+    case 2:
+      mgram_reg_kernel<2><<<nblk, NT, 0, st>>>(S, q, part);
+      m_iterate_kernel<2><<<1, NT, jsm, st>>>(part, nblk, q, ra, tol, max_iter, state, spatial,
+                                               dres, minfo, diag);
+      break;
+    case 3: {
+      constexpr size_t ring = sizeof(cplx) * MS_STAGES * 9 * MS_NTG;
+      KST_CUDA(ctx, cudaFuncSetAttribute(mgram_split_kernel<3, 3>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring));
+      mgram_split_kernel<3, 3><<<nblk, 3 * MS_NTG, ring, st>>>(S, q, rows_per, part);
+      m_iterate_kernel<3><<<1, NT, jsm, st>>>(part, nblk, q, ra, tol, max_iter, state, spatial,
+                                               dres, minfo, diag);
+    } break;
+    default:
+      mgram_kernel<4><<<nblk, NT, 0, st>>>(S, q, part);
+      m_iterate_kernel<4><<<1, NT, jsm, st>>>(part, nblk, q, ra, tol, max_iter, state, spatial,
+                                               dres, minfo, diag);
+      break;
+  }
+  ctx->launches += 1;  // + 1 in KST_LAUNCH: mgram + m_iterate
+  KST_LAUNCH(ctx);
+  // final b from the A that entered the last iteration (st->Aconj / st->na2)
+  cplx* vpart = (cplx*)part;
+  double* bpart = (double*)(vpart + (size_t)p * nvx * p);
+  KST_DISPATCH_P(p, (bstep_kernel<PP><<<dim3(nbb, q), NT, 0, st>>>(S, q, state, b, bpart)));
+  KST_LAUNCH(ctx);
+  KST_TRY(heig_top(ctx, b, q, rb, nullptr, tb_vectors, st, heig_ok, tb_vals_dev));
+  *dres_out = dres;
+  *diag_out = diag;
+  return KST_OK;
+}
+
 }  // namespace kst

@@ -444,3 +444,33 @@ def test_rank_deficient_temporal_basis_matches_oracle(n, rb, precision):
     filt = kst.build_filter("kron", estimate=kst.lr_kron_estimate(s, 1, rb))
     img = kst.detection_image(filt, cube, kst.make_doppler_grid(D), kst.make_spatial_grid(p, G))
     assert np.all(np.abs(img.values - ref) <= tight_tolerance(ref, m0, precision))
+
+
+def test_pipeline_optimistic_path_falls_back_exactly():
+    """kst_pipeline's host-sync-free form (q > 64) validates its assumptions on
+    the device and recomputes on the synchronous path when one fails: a
+    rank-deficient b (k_B < r_B), an all-zero frame, a non-finite frame. Each
+    outcome equals the step API / the oracle."""
+    from paper_1604_03622_b200 import scenes
+    p, q, D, G = 3, 96, 96, 16
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    base = scenes.bench_scene(p, q, 40, seed=5, movers=2).data[0]
+    m0 = orc.detect("kron", None, None, base, orc.doppler_grid(D), orc.spatial_grid(p, G)).max()
+    # common case (no fallback) and k_B < r_B (one bin: b of rank 1)
+    for cube, rb in ((base, 3), (base[:1], 3), (base[:2], 3)):
+        fit, ua, ub, ref = orc.pipeline(cube, 1, rb, D, G)
+        vals, info = kst.process_frame(cube, 1, rb, dopplers=dop, spatial_grid=grid)
+        assert info["iterations"] == fit.iterations and info["kb"] == ub.shape[1]
+        assert np.all(np.abs(vals - ref) <= 1e-5 * np.abs(ref) + 1e-6 * m0)
+    # all-zero frame: zero estimate, identity filter (src/lrkron.py:152-160)
+    z = np.zeros_like(base)
+    vals, info = kst.process_frame(z, 1, 3, dopplers=dop, spatial_grid=grid)
+    assert info["iterations"] == 0 and info["kb"] == 0 and not np.any(vals)
+    # non-finite frame: DataError as the reference's covariance validation
+    bad = base.copy()
+    bad[3, 1, 7] = np.nan
+    with pytest.raises(kst.DataError):
+        kst.process_frame(bad, 1, 3, dopplers=dop, spatial_grid=grid)
+    # and the context is usable afterwards
+    vals, info = kst.process_frame(base, 1, 3, dopplers=dop, spatial_grid=grid)
+    assert info["iterations"] >= 1

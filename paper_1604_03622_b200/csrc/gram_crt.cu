@@ -88,7 +88,11 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
     const cplx* __restrict__ X, int64_t n, int64_t npad, int64_t d, int64_t dpad,
     const int* __restrict__ expo, int beta, int8_t* __restrict__ R) {
   constexpr int NP = NEG ? 3 : 2;  // parts per modulus
-  __shared__ __align__(16) int8_t sb[NM][NP][CR_A][CR_KP];
+  // smem [column][modulus, part][row]: a column's NM NP row segments are
+  // contiguous, so phase 2's segment index maps to global memory with no
+  // division; +4 bytes per column keeps phase 1's byte stores conflict-free
+  constexpr int CC = NM * NP * CR_KP + 4;
+  __shared__ __align__(16) int8_t sb[CR_A * CC];
   const int64_t a0 = (int64_t)blockIdx.x * CR_A;
   const int tid = threadIdx.x;
   const int c = tid & (CR_A - 1), r_first = tid / CR_A;
@@ -132,9 +136,10 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
 #pragma unroll
       for (int i = 0; i < NM; ++i) {
         const uint8_t rr = crt_residue8<UNSIGNED>(modulus(i), hr, mr, lr);
-        sb[i][0][c][r] = (int8_t)rr;
-        sb[i][1][c][r] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hi, mi, li);
-        if (NEG) sb[i][NP - 1][c][r] = (int8_t)(rr ? (uint8_t)(modulus(i) - rr) : (uint8_t)0);
+        int8_t* sp = sb + c * CC + (i * NP) * CR_KP + r;
+        sp[0] = (int8_t)rr;
+        sp[CR_KP] = (int8_t)crt_residue8<UNSIGNED>(modulus(i), hi, mi, li);
+        if (NEG) sp[2 * CR_KP] = (int8_t)(rr ? (uint8_t)(modulus(i) - rr) : (uint8_t)0);
       }
     }
     if (sub + 1 < CR_SUB) {  // prefetch the next sub-block
@@ -147,12 +152,13 @@ __global__ void __launch_bounds__(256) crt_residue_kernel(
     __syncthreads();
     const int64_t k = kb0 + 4 * lw;
     if (k < npad) {  // npad is a multiple of 16: whole words only
-      for (int seg = tid >> 4; seg < CR_A * NM * NP; seg += 16) {
-        const int cc = seg / (NP * NM), rem = seg % (NP * NM), i = rem / NP, part = rem % NP;
-        const int64_t aa = a0 + cc;
-        if (aa >= dpad) continue;
-        *(uint32_t*)(R + (((size_t)aa * NM + i) * NP + part) * npad + k) =
-            *(const uint32_t*)&sb[i][part][cc][4 * lw];
+      // segment seg = (column cc, modulus i, part): R row ((a0 + cc) NM + i) NP
+      // + part = a0 NM NP + seg
+      int8_t* dst = R + (size_t)a0 * NM * NP * npad + k;
+      const int segs = (int)(dpad - a0 < CR_A ? dpad - a0 : CR_A) * NM * NP;
+      for (int seg = tid >> 4; seg < segs; seg += 16) {
+        const int cc = seg / (NP * NM), rem = seg - cc * (NP * NM);
+        *(uint32_t*)(dst + (size_t)seg * npad) = *(const uint32_t*)&sb[cc * CC + rem * CR_KP + 4 * lw];
       }
     }
     __syncthreads();

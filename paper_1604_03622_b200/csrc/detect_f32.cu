@@ -87,7 +87,16 @@ __constant__ float c_w4[F32_MAXG / 4][F32_MAXP][2];
 // wt[(u-1) h + (r-1)] = W_R^{u r mod R} = (cos, -sin) (warp-uniform
 // addresses: broadcast reads). ctw (Cooley-Tukey b-dim stages):
 // W_F^{r k1} = ctw[(r k1) mod F].
-template <int R, int ST = 0>  // ST > 0: compile-time element stride (fixed plans)
+// W_R^m = (cos, -sin)(2 pi m / R), m < R, of the fixed plan's factors: with
+// the output loop fully unrolled every twiddle is a constant-bank operand
+__constant__ float2 c_w3[3], c_w23[23], c_w29[29];
+template <int R>
+__device__ __forceinline__ float2 cw(int m) {
+  return R == 3 ? c_w3[m] : R == 23 ? c_w23[m] : c_w29[m];
+}
+
+template <int R, int ST = 0, bool CT = false>  // ST > 0: compile-time element stride (fixed
+                                               // plans); CT: constant-bank twiddles, unrolled u
 __device__ __forceinline__ void pencil(float2* __restrict__ a, int base, int st_rt,
                                        const float2* __restrict__ wt,
                                        const float2* __restrict__ ctw, int twF, int k1) {
@@ -141,6 +150,28 @@ __device__ __forceinline__ void pencil(float2* __restrict__ a, int base, int st_
     xn.y = fmaf(sn, t[R / 2].y, xn.y);
     a[base + (R / 2) * st] = xn;
   }
+  if (CT) {  // same operations, twiddles from the constant bank
+#pragma unroll
+    for (int u = 1; u <= h; ++u) {
+      float ax = t[0].x, ay = t[0].y, bx = 0.0f, by = 0.0f;
+      if (even) {
+        const float sg = (u & 1) ? -1.0f : 1.0f;
+        ax = fmaf(sg, t[R / 2].x, ax);
+        ay = fmaf(sg, t[R / 2].y, ay);
+      }
+#pragma unroll
+      for (int r = 1; r <= h; ++r) {
+        const float2 wm = cw<R>((u * r) % R);  // (cos, -sin)
+        ax = fmaf(wm.x, t[r].x, ax);
+        ay = fmaf(wm.x, t[r].y, ay);
+        bx = fmaf(-wm.y, t[R - r].x, bx);
+        by = fmaf(-wm.y, t[R - r].y, by);
+      }
+      a[base + u * st] = make_float2(ax + by, ay - bx);        // A - iB
+      a[base + (R - u) * st] = make_float2(ax - by, ay + bx);  // A + iB
+    }
+    return;
+  }
 #pragma unroll 1
   for (int u = 1; u <= h; ++u) {
     float ax = t[0].x, ay = t[0].y, bx = 0.0f, by = 0.0f;
@@ -184,7 +215,7 @@ __device__ __forceinline__ void stage_fixed(float2* buf, int nr, int D, const fl
   for (int wi = threadIdx.x; wi < nr * NPEN; wi += F32_NT) {
     const int row = (wi >= NPEN) + (wi >= 2 * NPEN), pn = wi - row * NPEN;
     const int base = (pn / ST) * (R * ST) + pn % ST;
-    pencil<R, ST>(buf + (size_t)row * D, base, ST, wt, nullptr, 0, 0);
+    pencil<R, ST, true>(buf + (size_t)row * D, base, ST, wt, nullptr, 0, 0);
   }
 }
 
@@ -810,6 +841,22 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
         w4[g0][i][1] = (float)sinl(th);
       }
     KST_TRY(const_upload(ctx, (const void*)&c_w4, w4, sizeof(w4), st));
+  }
+  {  // constant-bank twiddles of the fixed plan's factors (same values as the W tables)
+    const long double two_pi = 2.0L * 3.141592653589793238462643383279502884L;
+    float2 w3[3], w23[23], w29[29];
+    auto fill = [&](float2* w, int R) {
+      for (int m = 0; m < R; ++m) {
+        const long double th = two_pi * m / R;
+        w[m] = make_float2((float)cosl(th), (float)-sinl(th));
+      }
+    };
+    fill(w3, 3);
+    fill(w23, 23);
+    fill(w29, 29);
+    KST_TRY(const_upload(ctx, (const void*)&c_w3, w3, sizeof(w3), st));
+    KST_TRY(const_upload(ctx, (const void*)&c_w23, w23, sizeof(w23), st));
+    KST_TRY(const_upload(ctx, (const void*)&c_w29, w29, sizeof(w29), st));
   }
   static int nsm = 0;
   if (!nsm) {

@@ -37,3 +37,17 @@ span = prev_end - t0
 print(f"frame span {span:.1f} us, busy {tot_busy:.1f} us, idle {sum(g for g, _ in gaps):.1f} us in {len(gaps)} gaps")
 for g, n in sorted(gaps, reverse=True)[:15]:
     print(f"  gap {g:7.1f} us before {n}")
+
+import collections  # noqa: E402
+agg = collections.OrderedDict()
+for e in evs:
+    nm = e.name
+    for tag in ("kernel", "Kernel"):
+        pass
+    key = nm.split("(")[0].split("<")[0].split("::")[-1][:40]
+    a = agg.setdefault(key, [0, 0.0])
+    a[0] += 1
+    a[1] += e.time_range.end - e.time_range.start
+print("warm per-kernel (us):")
+for k, (c, v) in sorted(agg.items(), key=lambda x: -x[1][1])[:24]:
+    print(f"  {k:42s} {c:3d} {v:9.1f}")

@@ -287,12 +287,12 @@ __device__ __forceinline__ float dft_cand(const float2 (&y)[F32_MAXP], int P, in
 }
 
 // pixel d: Y'_a[d] - sum_k c_ak U^_k[d], y = Q Y', candidates, max |z| -> f64
-template <int NR>
+template <int NR, int PF = 0>  // PF > 0: compile-time channel count
 __device__ __forceinline__ void pixel(const float2* __restrict__ src, int D, int ps, int d,
                                       const float2 (&uf)[F32_MAXKB], const float2* cf,
                                       const float2* s_q, const float2* s_h, const F32Args& fa,
                                       double* __restrict__ vrow) {
-  const int P = fa.P, kb = fa.kb;
+  const int P = PF > 0 ? PF : fa.P, kb = fa.kb;
   float2 yq[NR];
 #pragma unroll
   for (int a = 0; a < NR; ++a) yq[a] = src[(size_t)a * D + ps];
@@ -351,15 +351,16 @@ __device__ __forceinline__ void pixel(const float2* __restrict__ src, int D, int
 // (FP64), accumulate the temporal coefficients (FP64) and scatter y' (c64)
 // into `dst` at the prime-factor input positions. Ends with a barrier (OR of
 // the non-finite test).
-template <int NR>
+template <int NR, int PF = 0>  // PF > 0: compile-time channel count
 __device__ __forceinline__ void load_bin(
-    const cplx* __restrict__ cube, int64_t mload, int P, int q, int D, int kb,
+    const cplx* __restrict__ cube, int64_t mload, int P_rt, int q, int D, int kb,
     const cplx* __restrict__ ub, const double2* s_qh, const uint16_t* pos_in,
     const uint16_t* pos_out, float2* dst, double (&acc)[NR * F32_MAXKB][2], int64_t mpix,
     const float2* src, const float2* cf, const float2* s_q, const float2* s_h,
     const float2* __restrict__ ubf, const F32Args& fa, double* __restrict__ values,
     int* __restrict__ nonfinite) {
   constexpr int NC = NR * F32_MAXKB;
+  const int P = PF > 0 ? PF : P_rt;
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = 0.0;
   int bad = 0;
@@ -386,7 +387,7 @@ __device__ __forceinline__ void load_bin(
         uf[k] = ufn[k];
         ufn[k] = (k < kb && tn < D) ? __ldg(&ubf[(size_t)k * D + tn]) : make_float2(0.0f, 0.0f);
       }
-      pixel<NR>(src, D, pos_out[t], t, uf, cf, s_q, s_h, fa, values + mpix * D);
+      pixel<NR, PF>(src, D, pos_out[t], t, uf, cf, s_q, s_h, fa, values + mpix * D);
     }
     if (mload < 0) continue;
     double2 yq[NR];
@@ -530,8 +531,9 @@ __global__ void f32_spec_kernel(const cplx* __restrict__ in, float2* __restrict_
 
 // Dynamic shared memory: two NR x D c64 row buffers | W tables (nw c64) |
 // pos_in, pos_out (D u16 each) | pencil bases (nbase u16).
-// PL = 0: any plan (stages from c_f32); PL = 1: D = 2001 = 3 x 23 x 29
-// (the Gotcha Doppler bank), every stage a compile-time instantiation
+// PL = 0: any plan (stages from c_f32); PL = 1: P = 3 channels and
+// D = 2001 = 3 x 23 x 29 (the Gotcha frame), every stage and channel loop a
+// compile-time instantiation
 template <int NR, int PL>
 __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
     const cplx* __restrict__ cube, int64_t n, const cplx* __restrict__ ub,
@@ -577,8 +579,8 @@ __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
   if (m >= n) return;
   {  // prologue: bin m0 -> bufs[0]
     double acc[NC][2];
-    load_bin<NR>(cube, m, P, q, D, kb, ub, s_qh, pos_in, pos_out, bufs[0], acc, -1, nullptr,
-                 s_cf[0], s_q, s_h, ubf, fa, values, nonfinite);
+    load_bin<NR, PL == 1 ? 3 : 0>(cube, m, P, q, D, kb, ub, s_qh, pos_in, pos_out, bufs[0], acc,
+                                  -1, nullptr, s_cf[0], s_q, s_h, ubf, fa, values, nonfinite);
     reduce_coef<NR, NV>(acc, red, kb, s_c, s_cf[0]);
   }
   int cur = 0;
@@ -601,8 +603,9 @@ __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
     if (tid == 0 && mn + g < n) prefetch_bin(cube, mn + g, P, q);
     double acc[NC][2];
     // pixels of bin m (+ the load pass of bin mn when it exists)
-    load_bin<NR>(cube, mn < n ? mn : -1, P, q, D, kb, ub, s_qh, pos_in, pos_out, bufs[cur ^ 1],
-                 acc, m, bufs[cur], s_cf[cur], s_q, s_h, ubf, fa, values, nonfinite);
+    load_bin<NR, PL == 1 ? 3 : 0>(cube, mn < n ? mn : -1, P, q, D, kb, ub, s_qh, pos_in, pos_out,
+                                  bufs[cur ^ 1], acc, m, bufs[cur], s_cf[cur], s_q, s_h, ubf, fa,
+                                  values, nonfinite);
     if (mn >= n) break;
     reduce_coef<NR, NV>(acc, red, kb, s_c, s_cf[cur ^ 1]);
   }
@@ -868,7 +871,7 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
   // the Gotcha Doppler bank has a compile-time plan (stage order 3, 23, 29)
   static const bool fixed_on = !(getenv("KST_F32_FIXED") && atoi(getenv("KST_F32_FIXED")) == 0);
   const F32Plan& pl = cp.plan;
-  const int PLv = (fixed_on && D == 2001 && pl.nst == 3 && pl.s[0].R == 3 && pl.s[0].st == 667 &&
+  const int PLv = (fixed_on && p == 3 && D == 2001 && pl.nst == 3 && pl.s[0].R == 3 && pl.s[0].st == 667 &&
                    pl.s[1].R == 23 && pl.s[1].st == 29 && pl.s[2].R == 29 && pl.s[2].st == 1)
                       ? 1
                       : 0;

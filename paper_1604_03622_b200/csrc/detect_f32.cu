@@ -292,7 +292,7 @@ __device__ __forceinline__ void pixel(const float2* __restrict__ src, int D, int
                                       const float2 (&uf)[F32_MAXKB], const float2* cf,
                                       const float2* s_q, const float2* s_h, const F32Args& fa,
                                       double* __restrict__ vrow) {
-  const int P = PF > 0 ? PF : fa.P, kb = fa.kb;
+  const int P = PF > 0 ? PF : fa.P, kb = PF > 0 ? F32_MAXKB : fa.kb;
   float2 yq[NR];
 #pragma unroll
   for (int a = 0; a < NR; ++a) yq[a] = src[(size_t)a * D + ps];
@@ -361,6 +361,7 @@ __device__ __forceinline__ void load_bin(
     int* __restrict__ nonfinite) {
   constexpr int NC = NR * F32_MAXKB;
   const int P = PF > 0 ? PF : P_rt;
+  if (PF > 0) kb = F32_MAXKB;  // the fixed plan also fixes k_B = 3
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = 0.0;
   int bad = 0;
@@ -531,9 +532,9 @@ __global__ void f32_spec_kernel(const cplx* __restrict__ in, float2* __restrict_
 
 // Dynamic shared memory: two NR x D c64 row buffers | W tables (nw c64) |
 // pos_in, pos_out (D u16 each) | pencil bases (nbase u16).
-// PL = 0: any plan (stages from c_f32); PL = 1: P = 3 channels and
-// D = 2001 = 3 x 23 x 29 (the Gotcha frame), every stage and channel loop a
-// compile-time instantiation
+// PL = 0: any plan (stages from c_f32); PL = 1: P = 3 channels, k_B = 3 and
+// D = 2001 = 3 x 23 x 29 (the Gotcha frame), every stage, channel and basis
+// loop a compile-time instantiation
 template <int NR, int PL>
 __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
     const cplx* __restrict__ cube, int64_t n, const cplx* __restrict__ ub,
@@ -545,7 +546,8 @@ __global__ void __launch_bounds__(F32_NT, KST_F32_MINB) detect_f32_kernel(
   constexpr int NC = NR * F32_MAXKB;  // coefficient count (complex)
   constexpr int NV = NC * 2 <= 8 ? 8 : NC * 2 <= 16 ? 16 : 32;
   extern __shared__ __align__(16) unsigned char f32_smem[];
-  const int D = fa.D, q = fa.q, P = fa.P, kb = fa.kb;
+  const int D = PL == 1 ? 2001 : fa.D, q = fa.q, P = PL == 1 ? 3 : fa.P,
+            kb = PL == 1 ? F32_MAXKB : fa.kb;
   float2* buf = (float2*)f32_smem;
   float2* s_wt = buf + (size_t)2 * NR * D;
   uint16_t* pos_in = (uint16_t*)(s_wt + c_f32.nw);
@@ -871,7 +873,8 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
   // the Gotcha Doppler bank has a compile-time plan (stage order 3, 23, 29)
   static const bool fixed_on = !(getenv("KST_F32_FIXED") && atoi(getenv("KST_F32_FIXED")) == 0);
   const F32Plan& pl = cp.plan;
-  const int PLv = (fixed_on && p == 3 && D == 2001 && pl.nst == 3 && pl.s[0].R == 3 && pl.s[0].st == 667 &&
+  const int PLv = (fixed_on && p == 3 && kb == F32_MAXKB && D == 2001 && pl.nst == 3 &&
+                   pl.s[0].R == 3 && pl.s[0].st == 667 &&
                    pl.s[1].R == 23 && pl.s[1].st == 29 && pl.s[2].R == 29 && pl.s[2].st == 1)
                       ? 1
                       : 0;

@@ -482,6 +482,9 @@ constexpr int MS_NTG = 128;  // threads per group = positions per tile
 #ifndef KST_MS_STAGES
 #define KST_MS_STAGES 4
 #endif
+#ifndef KST_MS_NG
+#define KST_MS_NG 2  // thread groups splitting M's upper triangle (P = 3; A/B: 2 159 us, 3 169, 4 177)
+#endif
 constexpr int MS_STAGES = KST_MS_STAGES;
 // chunk bounds: group 0 (which also carries the scans) takes a smaller share
 __host__ __device__ constexpr int ms_bound(int E, int NG, int g) {
@@ -753,9 +756,9 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
       case 3:
       {
         constexpr size_t ring = sizeof(cplx) * MS_STAGES * 9 * MS_NTG;
-        KST_CUDA(ctx, cudaFuncSetAttribute(mgram_split_kernel<3, 3>,
+        KST_CUDA(ctx, cudaFuncSetAttribute(mgram_split_kernel<3, KST_MS_NG>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring));
-        mgram_split_kernel<3, 3><<<nblk, 3 * MS_NTG, ring, st>>>(S, q, rows_per, mpart);
+        mgram_split_kernel<3, KST_MS_NG><<<nblk, KST_MS_NG * MS_NTG, ring, st>>>(S, q, rows_per, mpart);
       }
         m_iterate_kernel<3><<<1, NT, jsm, st>>>(mpart, nblk, q, ra, tol, max_iter, state, spatial,
                                                  dres, minfo, (double*)(small + sizeof(IterState)));
@@ -952,9 +955,9 @@ int lrkron_async(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, doub
       break;
     case 3: {
       constexpr size_t ring = sizeof(cplx) * MS_STAGES * 9 * MS_NTG;
-      KST_CUDA(ctx, cudaFuncSetAttribute(mgram_split_kernel<3, 3>,
+      KST_CUDA(ctx, cudaFuncSetAttribute(mgram_split_kernel<3, KST_MS_NG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring));
-      mgram_split_kernel<3, 3><<<nblk, 3 * MS_NTG, ring, st>>>(S, q, rows_per, part);
+      mgram_split_kernel<3, KST_MS_NG><<<nblk, KST_MS_NG * MS_NTG, ring, st>>>(S, q, rows_per, part);
       m_iterate_kernel<3><<<1, NT, jsm, st>>>(part, nblk, q, ra, tol, max_iter, state, spatial,
                                                dres, minfo, diag);
     } break;

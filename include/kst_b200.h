@@ -206,6 +206,12 @@ int kst_change(kst_ctx* ctx, const double* a, const double* b, int64_t count,
  * detection_image, on one cube, without materialising host copies.
  *   cube dev (n, p, q); values dev (groups, n, D); summary host (8 doubles):
  *   [iterations, converged, ka, kb, last residual, 0, 0, 0]
+ * Common case (p <= 4, q > 64, rank_temporal <= 24, rank_temporal < q): the
+ * whole frame is enqueued without a host synchronisation (convergence, kept
+ * ranks and validity decided on the device) and ONE synchronisation reads
+ * the outcome; a frame whose device checks fail is recomputed on the
+ * synchronous path (env KST_PIPE_ASYNC=0 forces it), so results and errors
+ * are the same either way.
  */
 int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
                  int rank_spatial, int rank_temporal, double tol, int max_iter,

@@ -10,6 +10,10 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef KST_JAC_BLOCK
+#define KST_JAC_BLOCK 0  // 1: the block rounds for n = 3 as well (A/B)
+#endif
+
 namespace kstj {
 
 constexpr int kMaxN = 64;
@@ -80,12 +84,100 @@ __device__ inline void jac_load_sym(JacSmem& j, const cplx* M, int ldm, int n, d
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- n = 3, one thread
+// For n = 3 the tournament has one real pair per round -- (0,1), (0,2),
+// (1,2) -- so a sweep is three sequential rotations. One thread runs them on
+// registers with compile-time indices: the same parameter formulas,
+// thresholds, column-then-row update and exact 2x2 diagonal as the block
+// rounds, without their four barriers per round (the P x P spatial
+// eigenproblems of every LR-Kron iteration and L-mode window).
+template <int P_, int Q_>
+__device__ __forceinline__ bool jac3_rot(cplx (&a)[3][3], cplx (&v)[3][3], double fro) {
+  const double app = a[P_][P_].x, aqq = a[Q_][Q_].x;
+  const cplx apq = a[P_][Q_];
+  const double r2 = apq.x * apq.x + apq.y * apq.y;
+  const double thr2 = fmax(4.84e-32 * fabs(app) * fabs(aqq), 1e-600 + 1e-30 * fro * fro);
+  if (!(r2 > thr2)) return false;
+  const double rinv = rsqrt(r2);
+  const double r = r2 * rinv;
+  const double ec = apq.x * rinv, es = apq.y * rinv;
+  const double tau = (aqq - app) * (0.5 * rinv);
+  const double t = copysign(1.0, tau) / (fabs(tau) + sqrt(fma(tau, tau, 1.0)));
+  const double c = rsqrt(fma(t, t, 1.0));
+  const double sn = t * c;
+  const cplx emi = cmk(ec, -es), epi = cmk(ec, es);
+#pragma unroll
+  for (int row = 0; row < 3; ++row) {  // A <- A U, V <- V U on columns (P_, Q_)
+    {
+      const cplx xp = a[row][P_], wq = cmul(emi, a[row][Q_]);
+      a[row][P_] = cmk(c * xp.x - sn * wq.x, c * xp.y - sn * wq.y);
+      a[row][Q_] = cmk(sn * xp.x + c * wq.x, sn * xp.y + c * wq.y);
+    }
+    {
+      const cplx xp = v[row][P_], wq = cmul(emi, v[row][Q_]);
+      v[row][P_] = cmk(c * xp.x - sn * wq.x, c * xp.y - sn * wq.y);
+      v[row][Q_] = cmk(sn * xp.x + c * wq.x, sn * xp.y + c * wq.y);
+    }
+  }
+#pragma unroll
+  for (int col = 0; col < 3; ++col) {  // A <- U^H A on rows (P_, Q_)
+    const cplx xp = a[P_][col], wq = cmul(epi, a[Q_][col]);
+    a[P_][col] = cmk(c * xp.x - sn * wq.x, c * xp.y - sn * wq.y);
+    a[Q_][col] = cmk(sn * xp.x + c * wq.x, sn * xp.y + c * wq.y);
+  }
+  a[P_][P_] = cmk(app - t * r, 0.0);
+  a[Q_][Q_] = cmk(aqq + t * r, 0.0);
+  a[P_][Q_] = cmk(0.0, 0.0);
+  a[Q_][P_] = cmk(0.0, 0.0);
+  return true;
+}
+
+static __device__ __noinline__ void jac3_thread(JacSmem& j) {
+  cplx a[3][3], v[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      a[r][c] = j.A[r * j.ld + c];
+      v[r][c] = j.V[r * j.ld + c];
+    }
+  double f = 0.0;
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) f += cabs2(a[r][c]);
+  const double fro = sqrt(f);
+  int sweeps = 0;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    bool any = jac3_rot<0, 1>(a, v, fro);
+    any |= jac3_rot<0, 2>(a, v, fro);
+    any |= jac3_rot<1, 2>(a, v, fro);
+    sweeps = sweep + 1;
+    if (!any) break;
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      j.A[r * j.ld + c] = a[r][c];
+      j.V[r * j.ld + c] = v[r][c];
+    }
+    j.val[r] = a[r][r].x;
+  }
+  j.flag[1] = sweeps;  // diagnostic: sweeps used
+}
+
 // Run Jacobi sweeps on j.A (Hermitian), accumulating j.V. On return
 // j.val holds the (unsorted) diagonal.
 __device__ inline void jac_sweeps(JacSmem& j, int n) {
   const int tid = threadIdx.x, nt = blockDim.x;
   if (n == 1) {
     if (tid == 0) j.val[0] = j.A[0].x;
+    __syncthreads();
+    return;
+  }
+  if (n == 3 && !KST_JAC_BLOCK) {
+    if (tid == 0) jac3_thread(j);
     __syncthreads();
     return;
   }

@@ -317,6 +317,6 @@ int spectra(kst_ctx* ctx, const cplx* x, int64_t rows, int q, const double* dop_
 bool detect_f32_supported(int p, int q, int ka, int kb, int mode, int spatial, int D, int G);
 int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
                const cplx* ub, int kb, int mode, int spatial, int D, const cplx* ubspec,
-               const cplx* hconj, const cplx* grid_host, int G, bool dft, double* values,
-               int* flag, cudaStream_t st);
+               const cplx* tw, const cplx* hconj, const cplx* grid_host, int G, bool dft,
+               double* values, int* flag, cudaStream_t st);
 }  // namespace kst

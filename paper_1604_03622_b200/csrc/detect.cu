@@ -1193,7 +1193,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     configured = 226 * 1024;
   }
-  if (kb_used > 0) {
+  if (kb_used > 0 && !f32) {  // (the FP32 kernel takes its basis spectra by a direct DFT)
     transpose_kernel<<<cdiv((int64_t)q * kb_used, 256), 256, 0, st>>>(ub, q, kb_used, ubT);
     KST_LAUNCH(ctx);
     // spectra of the temporal basis columns (coefficients unused)
@@ -1204,7 +1204,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   if (f32) {
     const bool dft = G % 4 == 0 && dft_grid(grid_host, G, p);
     const int rc = detect_f32(ctx, cube, n, p, q, has_a ? ua : nullptr, has_a ? ka : 0, ub, kb_used,
-                              mode, spatial, D, ubspec, hconj, grid_host, G, dft, values,
+                              mode, spatial, D, nullptr, tw, hconj, grid_host, G, dft, values,
                               check_finite ? flag : nullptr, st);
     if (rc != KST_OK) return rc == -1 ? set_err(ctx, KST_ERR_CUDA, "detect_f32: plan rejected") : rc;
   } else if (fused) {

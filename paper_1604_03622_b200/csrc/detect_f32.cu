@@ -525,6 +525,37 @@ __global__ void f32_q_kernel(const cplx* __restrict__ ua, int P, int ka, int spa
   }
 }
 
+// Basis spectra for the FP32 transform straight from the time-domain basis:
+// U^_k[d] = sum_t U_B[t, k] W_D^{t d} (uniform grid, exact index t d mod D
+// into the FP64 twiddle table), FP64 sums rounded once to c64. CTA = 16
+// Dopplers x 32 pulse chunks, the chunks summed in fixed order (replaces the
+// transpose + one-CTA-per-row FFT + conversion: 3 launches, ~26 us).
+constexpr int BD_D = 8, BD_C = 32;
+__global__ void __launch_bounds__(BD_D * BD_C) f32_basis_dft_kernel(
+    const cplx* __restrict__ ub, int kb, int q, const cplx* __restrict__ tw, int D,
+    float2* __restrict__ ubf) {
+  __shared__ cplx part[BD_C][BD_D];
+  const int dl = threadIdx.x % BD_D, ch = threadIdx.x / BD_D;
+  const int d = blockIdx.x * BD_D + dl, k = blockIdx.y;
+  const int tl = (q + BD_C - 1) / BD_C, t0 = ch * tl, t1 = min(q, t0 + tl);
+  cplx acc = cmk(0, 0);
+  if (d < D) {
+    int idx = (int)(((int64_t)t0 * d) % D);
+    for (int t = t0; t < t1; ++t) {
+      cfma(acc, ub[(size_t)t * kb + k], tw[idx]);
+      idx += d;
+      if (idx >= D) idx -= D;
+    }
+  }
+  part[ch][dl] = acc;
+  __syncthreads();
+  if (ch == 0 && d < D) {
+    cplx s = part[0][dl];
+    for (int c = 1; c < BD_C; ++c) s = cadd(s, part[c][dl]);
+    ubf[(size_t)k * D + d] = make_float2((float)s.x, (float)s.y);
+  }
+}
+
 __global__ void f32_spec_kernel(const cplx* __restrict__ in, float2* __restrict__ out, int count) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) out[i] = make_float2((float)in[i].x, (float)in[i].y);
@@ -783,8 +814,8 @@ bool detect_f32_supported(int p, int q, int ka, int kb, int mode, int spatial, i
 // problem (the caller runs the FP64 path).
 int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* ua, int ka,
                const cplx* ub, int kb, int mode, int spatial, int D, const cplx* ubspec,
-               const cplx* hconj, const cplx* grid_host, int G, bool dft, double* values,
-               int* flag, cudaStream_t st) {
+               const cplx* tw, const cplx* hconj, const cplx* grid_host, int G, bool dft,
+               double* values, int* flag, cudaStream_t st) {
   (void)grid_host;
   if (!detect_f32_supported(p, q, ka, kb, mode, spatial, D, G)) return -1;
   const int nr = (mode == 1 || !spatial) ? p : p - ka;
@@ -818,8 +849,12 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
     ctx->f32_D = D;
   }
   KST_TRY(const_upload(ctx, (const void*)&c_f32, &cp.plan, sizeof(F32Plan), st));
-  if (kb > 0) {
+  if (kb > 0 && ubspec) {
     f32_spec_kernel<<<cdiv((int64_t)kb * D, 256), 256, 0, st>>>(ubspec, ubf, kb * D);
+    KST_LAUNCH(ctx);
+  } else if (kb > 0) {  // spectra straight from the basis (uniform grid twiddles)
+    f32_basis_dft_kernel<<<dim3((unsigned)cdiv(D, BD_D), (unsigned)kb), BD_D * BD_C, 0, st>>>(
+        ub, kb, q, tw, D, ubf);
     KST_LAUNCH(ctx);
   }
   const int spat = (mode != 1 && spatial && ka > 0) ? 1 : 0;

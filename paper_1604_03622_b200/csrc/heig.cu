@@ -342,20 +342,29 @@ __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict
   if (threadIdx.x < s) Z[(size_t)picked[threadIdx.x] * s + threadIdx.x] = cmk(1.0, 0.0);
 }
 
-// Device form of heig_top's round-0 convergence test (host loop below): every
-// wanted Ritz pair with residual <= 1e-12 max|theta|, or <= 1e-9 max|theta|
-// and <= 1e-8 of its gap; kept > 0. Same sums in the same order as the host.
+// heig_top's Rayleigh-Ritz convergence test, on the device for both the
+// synchronous loop and the sync-free form: res_red[k] = sum over the row-
+// block partials of the k-th squared residual (one warp, fixed-order lane
+// sums + xor tree: both paths see identical values), then every wanted pair
+// with residual <= 1e-12 max|theta|, or <= 1e-9 max|theta| and <= 1e-8 of
+// its gap, and kept > 0 -> *ok = 1.
 __global__ void rr_check_kernel(const double* __restrict__ res_part, int nup, int r,
                                 const double* __restrict__ th, int s, const int* __restrict__ info,
-                                int* __restrict__ ok) {
-  if (threadIdx.x != 0) return;
+                                double* __restrict__ res_red, int* __restrict__ ok) {
+  const int lane = threadIdx.x & 31;
+  for (int k = 0; k < r; ++k) {
+    double acc = 0.0;
+    for (int b = lane; b < nup; b += 32) acc += res_part[(size_t)b * r + k];
+    acc = warp_sum(acc);
+    if (lane == 0) res_red[k] = acc;
+  }
+  __syncwarp();
+  if (lane != 0) return;
   double tmax = 0.0;
   for (int k = 0; k < s; ++k) tmax = fmax(tmax, fabs(th[k]));
   bool all_ok = true;
   for (int k = 0; k < r; ++k) {
-    double acc = 0.0;
-    for (int b = 0; b < nup; ++b) acc += res_part[(size_t)b * r + k];
-    const double res = sqrt(acc);
+    const double res = sqrt(res_red[k]);
     double gap = 1e300;
     for (int jx = 0; jx < s; ++jx)
       if (jx != k) gap = fmin(gap, fabs(th[k] - th[jx]));
@@ -1008,11 +1017,11 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   const int nblk = std::min((n + K4_ROWS - 1) / K4_ROWS, 32);
   const int nup = (n + 7) / 8;
   size_t bytes = sizeof(cplx) * (nb * 5 + (size_t)s * s * 2) +
-                 sizeof(double) * ((size_t)nup * r + 2 * s) + sizeof(int) * 8 + 256;
+                 sizeof(double) * ((size_t)nup * r + 2 * s + r + 4) + sizeof(int) * 8 + 256;
   char* base = (char*)ws_get(ctx, WS_EIG, bytes);
   cplx* partial = (cplx*)ws_get(ctx, WS_EIG2, sizeof(cplx) * (size_t)nblk * 2 * s * s +
                                                   sizeof(double) * (size_t)nup * r + 64);
-  double* hres = (double*)pinned_get(ctx, sizeof(double) * ((size_t)nup * r + 2 * s + 8));
+  double* hres = (double*)pinned_get(ctx, sizeof(double) * (2 * s + r + 8));
   if (!base || !partial || !hres) return set_err(ctx, KST_ERR_CUDA, "heig_top: workspace");
   cplx* Z = (cplx*)base;
   cplx* Y = Z + nb;
@@ -1021,11 +1030,14 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
   cplx* X = Zn + nb;
   cplx* Cm = X + nb;
   cplx* Qm = Cm + s * s;
-  // [residual partials | theta | vout | info] contiguous: one readback per iteration
+  // [residual partials | theta | vout | info (2 ints) | reduced residuals | ok]:
+  // theta .. ok contiguous, one readback per Rayleigh-Ritz round
   double* res_part = (double*)(Qm + s * s);
   double* theta = res_part + (size_t)nup * r;
   double* vout = theta + s;
   int* info = (int*)(vout + s);
+  double* res_red = (double*)(info + 2);
+  int* ok_loop = (int*)(res_red + r);
   const size_t small_smem = ((jac_smem_bytes(s) + 15) / 16) * 16 + sizeof(cplx) * 4 * s * s;
   static bool small_attr = false;
   if (!small_attr) {
@@ -1072,7 +1084,7 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
     cplx* Zcur = Z;
     KST_TRY(step(Zcur, Y, Y2, 0));
-    rr_check_kernel<<<1, 32, 0, st>>>(res_part, nup, r, theta, s, info, ok_dev);
+    rr_check_kernel<<<1, 32, 0, st>>>(res_part, nup, r, theta, s, info, res_red, ok_dev);
     KST_LAUNCH(ctx);
     finalize_top_kernel<<<1, 1024, 0, st>>>(X, n, s, r, theta, vout, vectors);
     KST_LAUNCH(ctx);
@@ -1088,13 +1100,15 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
     cplx* Zcur = Z;
     KST_TRY(step(Zcur, Y, Y2, 0));  // X = Ritz vectors of span(Zcur); Z <- orth(B^2 Zcur)
-    KST_CUDA(ctx, cudaMemcpyAsync(hres, res_part,
-                                  sizeof(double) * ((size_t)nup * r + 2 * s) + 2 * sizeof(int),
+    rr_check_kernel<<<1, 32, 0, st>>>(res_part, nup, r, theta, s, info, res_red, ok_loop);
+    KST_LAUNCH(ctx);
+    KST_CUDA(ctx, cudaMemcpyAsync(hres, theta, sizeof(double) * (2 * s + r) + 2 * sizeof(int),
                                   cudaMemcpyDeviceToHost, st));
     KST_CUDA(ctx, cudaStreamSynchronize(st));
-    const double* th = hres + (size_t)nup * r;
-    const int kept = *(int*)(hres + (size_t)nup * r + 2 * s);
-    const int path = *((int*)(hres + (size_t)nup * r + 2 * s) + 1);
+    const double* th = hres;
+    const int kept = *(int*)(hres + 2 * s);
+    const int path = *((int*)(hres + 2 * s) + 1);
+    const double* hred = hres + 2 * s + 1;  // the device-reduced squared residuals
     double tmax = 0.0, worst = 0.0;
     for (int k = 0; k < s; ++k) tmax = std::max(tmax, std::fabs(th[k]));
     // Converged when every wanted Ritz pair has residual <= 1e-12 max|theta|
@@ -1102,9 +1116,7 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     // other Ritz values: eigenvector error <= residual / gap <= 1e-8.
     bool all_ok = true;
     for (int k = 0; k < r; ++k) {
-      double acc = 0.0;
-      for (int b = 0; b < nup; ++b) acc += hres[(size_t)b * r + k];
-      const double res = std::sqrt(acc);
+      const double res = std::sqrt(hred[k]);
       worst = std::max(worst, res);
       double gap = 1e300;
       for (int jx = 0; jx < s; ++jx)

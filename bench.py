@@ -686,12 +686,26 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # The frame as a CUDA graph (FrameGraph: kst_pipeline_async captured once
+    # per cube buffer, one graph launch per frame, every decision on the
+    # device); KST_BENCH_GRAPH=0 times the direct kst_pipeline call instead.
+    # Profiling is on before the capture, so the stage marks are event-record
+    # nodes of the graph and every replay re-times its stages.
+    use_graph = os.environ.get("KST_BENCH_GRAPH", "1") != "0"
+    lib.kst_set_profiling(c, 1)
+    graphs = []
+    if use_graph:
+        from paper_1604_03622_b200.pipeline import FrameGraph
+        graphs = [FrameGraph(cb, ra, rb, dop, grid, out=out) for cb in cubes]
+
     def step(i):
-        kst.process_frame_device(cubes[i % 2], ra, rb, dop, grid, out=out, summary=summ)
+        if use_graph:
+            graphs[i % 2].replay()
+        else:
+            kst.process_frame_device(cubes[i % 2], ra, rb, dop, grid, out=out, summary=summ)
 
     for i in range(args.warmup):
         step(i)
-    lib.kst_set_profiling(c, 1)
     clocks = ClockSampler(local)
     clocks.start()
     times, stages, iters = [], [], []
@@ -709,8 +723,16 @@ def main():
         st = np.zeros(8)
         k = lib.kst_stage_times(c, st.ctypes.data_as(nat.C.c_void_p), 8)
         stages.append(st[:k].copy())
-        iters.append(int(summ[0]))
+        if use_graph:  # the device outcome record of this replay (ok, iterations, ...)
+            rec = graphs[i % 2].rec.cpu().numpy()
+            if rec[0] != 1.0:
+                raise RuntimeError("bench: a replayed frame left the sync-free form")
+            iters.append(int(rec[1]))
+        else:
+            iters.append(int(summ[0]))
     launches = lib.kst_launch_count(c) - launches0
+    if use_graph:  # host-side count is 0 for replays: kernels per captured frame
+        launches = sum(graphs[i % 2].launches for i in range(args.steps))
     lib.kst_set_profiling(c, 0)
 
     # end to end through the public API with pinned host buffers: every step
@@ -814,6 +836,9 @@ def main():
                             + ("; N > 1: each step's maps all-gathered over NCCL and the "
                                "gathered stack read back by rank 0" if world > 1 else "")},
             "gpu_launches": int(launches),
+            "frame_api": ("FrameGraph: kst_pipeline_async captured as one CUDA graph per cube "
+                          "buffer, one graph launch per frame" if use_graph else
+                          "process_frame_device (kst_pipeline, one host sync per frame)"),
             "clocks": clk,
         }
         if numpy_api is not None:

@@ -220,6 +220,31 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q,
                  void* stream);
 
 /*
+ * Sync-free half of kst_pipeline, for CUDA-graph capture of a frame: enqueues
+ * the common-case schedule (same arguments as kst_pipeline) with no host
+ * synchronisation and writes the device outcome record rec (device, 8
+ * doubles): [ok, iterations, converged, ka, kb, last residual, 0, 0]. When
+ * rec[0] != 1 an assumption of the sync-free form failed and values are not
+ * valid: recompute the frame with kst_pipeline. Returns KST_ERR_DIMENSION,
+ * with nothing enqueued, outside the common case (p <= 4, q > 64,
+ * 1 <= rank_temporal <= 24, rank_temporal < q). After one call with the same
+ * arguments (workspaces allocated, resident tables staged) a further call
+ * allocates nothing and can be captured with cudaStreamBeginCapture; the
+ * capture stays valid while kst_state_epoch() is unchanged.
+ */
+int kst_pipeline_async(kst_ctx* ctx, const double* cube, int64_t n, int p,
+                       int q, int rank_spatial, int rank_temporal, double tol,
+                       int max_iter, int kind, const double* dopplers, int D,
+                       const double* grid, int G, int groups, double* values,
+                       double* rec, void* stream);
+
+/* Resident-state epoch (process-wide): changes whenever device state a
+ * captured frame depends on changes outside the capture -- a workspace or
+ * pinned buffer reallocated, a constant bank uploaded, resident detection
+ * tables restaged. */
+long long kst_state_epoch(void);
+
+/*
  * Windowed (L-mode) estimator, one call for a run of windows (SURVEY.md §8
  * "L-mode definition"; the reference has no windowed mode -- each window is
  * its README sequence, pkg/README.md:144-161: sample_covariance

@@ -56,6 +56,9 @@ _SIGS = {
     "kst_chol_solve": (_i, [_vp, _vp, _i, _vp, _i64, _vp, _vp]),
     "kst_pipeline": (_i, [_vp, _vp, _i64, _i, _i, _i, _i, _d, _i, _i, _vp, _i, _vp, _i, _i, _vp,
                           _vp, _vp]),
+    "kst_pipeline_async": (_i, [_vp, _vp, _i64, _i, _i, _i, _i, _d, _i, _i, _vp, _i, _vp, _i, _i,
+                                _vp, _vp, _vp]),
+    "kst_state_epoch": (C.c_longlong, []),
 }
 
 KIND = {"kron": 0, "classical": 1}

@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -21,10 +22,18 @@ int set_err(kst_ctx* ctx, int code, const char* fmt, ...) {
   return code;
 }
 
+static std::atomic<long long> g_epoch{1};
+void epoch_bump(const char* why, long long tag) {
+  g_epoch.fetch_add(1);
+  static const bool dbg = getenv("KST_EPOCH_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "[kst] state epoch bump: %s %lld\n", why ? why : "?", tag);
+}
+
 void* ws_get(kst_ctx* ctx, int slot, size_t bytes) {
   auto& s = ctx->slots[slot];
   if (bytes == 0) bytes = 1;
   if (s.bytes >= bytes) return s.ptr;
+  epoch_bump("workspace", slot);
   if (s.ptr) {
     // in-flight kernels may still read the old buffer
     cudaDeviceSynchronize();
@@ -50,6 +59,7 @@ int const_upload(kst_ctx* ctx, const void* symbol, const void* src, size_t bytes
   std::lock_guard<std::mutex> lock(mu);
   auto& cur = held[{dev, symbol}];
   if (cur.size() == bytes && std::memcmp(cur.data(), src, bytes) == 0) return KST_OK;
+  epoch_bump("constant", (long long)(uintptr_t)symbol);
   const cudaError_t e = cudaMemcpyToSymbolAsync(symbol, src, bytes, 0, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) {
     cur.clear();
@@ -61,6 +71,7 @@ int const_upload(kst_ctx* ctx, const void* symbol, const void* src, size_t bytes
 
 void* pinned_get(kst_ctx* ctx, size_t bytes) {
   if (ctx->pinned_bytes >= bytes) return ctx->pinned;
+  epoch_bump("pinned", (long long)bytes);
   if (ctx->pinned) {
     cudaDeviceSynchronize();
     cudaFreeHost(ctx->pinned);
@@ -318,6 +329,75 @@ int kst_detect(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, const 
                      (cudaStream_t)stream);
 }
 
+// The sync-free form of a frame applies (p <= 4, q > 64 for heig_top's
+// block solver, r_b <= 24 and < q)
+static bool pipeline_async_ok(int p, int q, int rank_spatial, int rank_temporal, int max_iter) {
+  return rank_temporal != q && p <= 4 && q > 64 /* heig_top Jacobi limit */ && rank_spatial >= 1 &&
+         rank_spatial <= p && rank_temporal >= 1 && rank_temporal <= 24 && max_iter >= 1;
+}
+
+// Enqueue the whole frame with every decision (convergence, kept ranks,
+// validity) taken on the device; rec (device, 8 doubles) receives
+// [ok, iterations, converged, ka, kb, last residual]. No host
+// synchronisation, no allocation once the workspaces exist: capturable in a
+// CUDA graph after one call with the same arguments.
+static int pipeline_async_core(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int rank_spatial,
+                               int rank_temporal, double tol, int max_iter, int kind,
+                               const double* dopplers, int D, const double* grid, int G, int groups,
+                               double* values, double* rec_out, cudaStream_t st) {
+  const int64_t d = (int64_t)p * q;
+  cplx* S = (cplx*)ws_get(ctx, WS_S, sizeof(cplx) * d * d);
+  cplx* ubA = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);
+  // spatial (p^2) | ua (p^2) | Jacobi vectors (p^2) | values (p) | rec (8) | flags
+  char* sp = (char*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 3 + sizeof(double) * (p + 8) + 64);
+  if (!S || !ubA || !sp) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+  cplx* spA = (cplx*)sp;
+  cplx* uaA = spA + p * p;
+  cplx* vecA = uaA + p * p;
+  double* valA = (double*)(vecA + p * p);
+  double* rec = rec_out ? rec_out : valA + p;
+  int* flags = (int*)(valA + p + 8);
+  int* heig_ok = flags + 2;
+  stage_mark(ctx, 0, st);
+  KST_TRY(kst::scm(ctx, (const cplx*)cube, n, d, S, st));
+  stage_mark(ctx, 1, st);
+  const double* tbv_dev = nullptr;
+  const double* dres = nullptr;
+  const double* diag = nullptr;
+  KST_TRY(kst::lrkron_async(ctx, S, p, q, rank_spatial, rank_temporal, tol, max_iter, spA, ubA, heig_ok,
+                            &tbv_dev, &dres, &diag, st));
+  stage_mark(ctx, 2, st);
+  KST_TRY(kst::small_heig(ctx, spA, p, valA, vecA, st));
+  const int ka = rank_spatial;
+  spatial_basis_kernel<<<1, 32, 0, st>>>(spA, p, valA, vecA, ka, uaA, flags);
+  KST_LAUNCH(ctx);
+  stage_mark(ctx, 3, st);
+  KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, uaA, ka, ubA, rank_temporal, kind, 0, dopplers, D,
+                      (const cplx*)grid, G, groups, values, st, false));
+  stage_mark(ctx, 4, st);
+  pipeline_check_kernel<<<1, 32, 0, st>>>(tbv_dev, rank_temporal, dres, max_iter, diag, heig_ok, flags, ka,
+                                          rec);
+  KST_LAUNCH(ctx);
+  return KST_OK;
+}
+
+int kst_pipeline_async(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int rank_spatial,
+                       int rank_temporal, double tol, int max_iter, int kind, const double* dopplers,
+                       int D, const double* grid, int G, int groups, double* values, double* rec,
+                       void* stream) {
+  CTX_GUARD(ctx);
+  if (n < 1 || p < 1 || q < 1) return set_err(ctx, KST_ERR_DIMENSION, "pipeline: empty cube");
+  if (!rec) return set_err(ctx, KST_ERR_DIMENSION, "pipeline_async: rec buffer required");
+  if (!pipeline_async_ok(p, q, rank_spatial, rank_temporal, max_iter))
+    return set_err(ctx, KST_ERR_DIMENSION,
+                   "pipeline_async: shape outside the sync-free form (p <= 4, q > 64, "
+                   "1 <= rank_temporal <= 24, rank_temporal < q)");
+  return pipeline_async_core(ctx, cube, n, p, q, rank_spatial, rank_temporal, tol, max_iter, kind, dopplers,
+                             D, grid, G, groups, values, rec, (cudaStream_t)stream);
+}
+
+long long kst_state_epoch(void) { return g_epoch.load(); }
+
 int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int rank_spatial,
                  int rank_temporal, double tol, int max_iter, int kind, const double* dopplers,
                  int D, const double* grid, int G, int groups, double* values, double* summary,
@@ -326,55 +406,22 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t d = (int64_t)p * q;
   if (n < 1 || p < 1 || q < 1) return set_err(ctx, KST_ERR_DIMENSION, "pipeline: empty cube");
-  cplx* S = (cplx*)ws_get(ctx, WS_S, sizeof(cplx) * d * d);
-  cplx* spatial = (cplx*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 2 + 64);
-  if (!S || !spatial) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
-  cplx* ua = spatial + p * p;
-  stage_mark(ctx, 0, st);
-  KST_TRY(kst::scm(ctx, (const cplx*)cube, n, d, S, st));
-  stage_mark(ctx, 1, st);
-  // the temporal basis must survive until detection: dedicated slot
   const bool full_b = rank_temporal == q;
-  // Optimistic host-sync-free form of the common case (p <= 4, q > 64,
-  // r_b <= 24): estimator, bases and detection are enqueued back to back
-  // with every decision (convergence, kept ranks, validity) taken on the
-  // device; ONE synchronisation at the end reads the outcome. When any
-  // assumption fails (non-finite or zero S, a degenerate iterate, the
-  // eigensolver needing more than one round, k_A < r_A, k_B < r_B) the
+  // Optimistic host-sync-free form of the common case: estimator, bases and
+  // detection are enqueued back to back with every decision taken on the
+  // device (pipeline_async_core); ONE synchronisation reads the outcome.
+  // When any assumption fails (non-finite or zero S, a degenerate iterate,
+  // the eigensolver needing more than one round, k_A < r_A, k_B < r_B) the
   // frame is recomputed from S by the synchronous path below, so results
   // equal the synchronous path's either way.
   static const bool async_env = !(getenv("KST_PIPE_ASYNC") && atoi(getenv("KST_PIPE_ASYNC")) == 0);
-  if (async_env && !full_b && p <= 4 && q > 64 /* heig_top Jacobi limit */ && rank_spatial >= 1 &&
-      rank_spatial <= p && rank_temporal >= 1 && rank_temporal <= 24 && max_iter >= 1) {
-    cplx* ubA = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);
-    // spatial (p^2) | ua (p^2) | Jacobi vectors (p^2) | values (p) | rec (8) | flags
-    char* sp = (char*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 3 + sizeof(double) * (p + 8) + 64);
+  if (async_env && pipeline_async_ok(p, q, rank_spatial, rank_temporal, max_iter)) {
     double* hrec = (double*)pinned_get(ctx, 256);
-    if (!ubA || !sp || !hrec) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
-    cplx* spA = (cplx*)sp;
-    cplx* uaA = spA + p * p;
-    cplx* vecA = uaA + p * p;
-    double* valA = (double*)(vecA + p * p);
-    double* rec = valA + p;
-    int* flags = (int*)(rec + 8);
-    int* heig_ok = flags + 2;
-    const double* tbv_dev = nullptr;
-    const double* dres = nullptr;
-    const double* diag = nullptr;
-    KST_TRY(kst::lrkron_async(ctx, S, p, q, rank_spatial, rank_temporal, tol, max_iter, spA, ubA,
-                              heig_ok, &tbv_dev, &dres, &diag, st));
-    stage_mark(ctx, 2, st);
-    KST_TRY(kst::small_heig(ctx, spA, p, valA, vecA, st));
-    const int ka = rank_spatial;
-    spatial_basis_kernel<<<1, 32, 0, st>>>(spA, p, valA, vecA, ka, uaA, flags);
-    KST_LAUNCH(ctx);
-    stage_mark(ctx, 3, st);
-    KST_TRY(kst::detect(ctx, (const cplx*)cube, n, p, q, uaA, ka, ubA, rank_temporal, kind, 0,
-                        dopplers, D, (const cplx*)grid, G, groups, values, st, false));
-    stage_mark(ctx, 4, st);
-    pipeline_check_kernel<<<1, 32, 0, st>>>(tbv_dev, rank_temporal, dres, max_iter, diag, heig_ok,
-                                            flags, ka, rec);
-    KST_LAUNCH(ctx);
+    if (!hrec) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+    double* rec = (double*)ws_get(ctx, WS_PIPE_REC, 64 * sizeof(double));
+    if (!rec) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+    KST_TRY(pipeline_async_core(ctx, cube, n, p, q, rank_spatial, rank_temporal, tol, max_iter, kind,
+                                dopplers, D, grid, G, groups, values, rec, st));
     KST_CUDA(ctx, cudaMemcpyAsync(hrec, rec, sizeof(double) * 6, cudaMemcpyDeviceToHost, st));
     KST_CUDA(ctx, cudaStreamSynchronize(st));
     if (hrec[0] == 1.0) {
@@ -389,6 +436,16 @@ int kst_pipeline(kst_ctx* ctx, const double* cube, int64_t n, int p, int q, int 
       return KST_OK;
     }
     // an assumption failed: the synchronous path recomputes from S
+  }
+  cplx* S = (cplx*)ws_get(ctx, WS_S, sizeof(cplx) * d * d);
+  cplx* spatial = (cplx*)ws_get(ctx, WS_PIPE_SP, sizeof(cplx) * p * p * 3 + sizeof(double) * (p + 8) + 64);
+  if (!S || !spatial) return set_err(ctx, KST_ERR_CUDA, "pipeline: workspace");
+  cplx* ua = spatial + p * p;
+  const bool s_ready = async_env && pipeline_async_ok(p, q, rank_spatial, rank_temporal, max_iter);
+  if (!s_ready) {
+    stage_mark(ctx, 0, st);
+    KST_TRY(kst::scm(ctx, (const cplx*)cube, n, d, S, st));
+    stage_mark(ctx, 1, st);
   }
   // ub: the top-rb eigenvectors (q x rb), then the kept kb columns repacked (q x kb)
   cplx* ub = (cplx*)ws_get(ctx, WS_PIPE_UB, sizeof(cplx) * (size_t)q * rank_temporal * 2 + 64);

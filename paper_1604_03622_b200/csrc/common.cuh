@@ -113,7 +113,13 @@ inline void stage_mark(kst_ctx* ctx, int k, cudaStream_t st) {
   }
   if (!ctx->profiling || k >= 8) return;
   if (!ctx->ev[k]) cudaEventCreate(&ctx->ev[k]);
-  cudaEventRecord(ctx->ev[k], st);
+  // inside a CUDA-graph capture (FrameGraph) the marks become event-record
+  // nodes, so every replay re-times its stages
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ctx->ev[k], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ctx->ev[k], st);
   if (k + 1 > ctx->n_ev) ctx->n_ev = k + 1;
 }
 
@@ -142,7 +148,8 @@ enum WsSlot {
   WS_LM_W = 21,     // L-mode: banded snapshot Gram + row sums
   WS_LM_E = 22,     // L-mode: per-test-bin projection matrices + window info
   WS_LM_H = 23,     // L-mode: per-CTA eigen scratch (small Grams, residuals)
-  WS_DET32 = 24     // FP32 detection: prime-factor position maps
+  WS_DET32 = 24,    // FP32 detection: prime-factor position maps
+  WS_PIPE_REC = 25  // pipeline: device outcome record of the sync-free form
 };
 
 // Every extern "C" entry point runs on its context's device: the caller's
@@ -174,6 +181,12 @@ void* pinned_get(kst_ctx* ctx, size_t bytes);
 // host->device transfer, which costs tens of us when PCIe is saturated by a
 // cube upload).
 int const_upload(kst_ctx* ctx, const void* symbol, const void* src, size_t bytes, cudaStream_t st);
+// Resident-state epoch: bumped whenever device state that a captured CUDA
+// graph of a frame depends on changes outside the graph (a workspace or pinned
+// buffer reallocated, a constant bank uploaded, resident detection tables
+// restaged). kst_state_epoch exports it; a graph captured at epoch e replays
+// correctly while the epoch is still e.
+void epoch_bump(const char* why = nullptr, long long tag = 0);
 
 int set_err(kst_ctx* ctx, int code, const char* fmt, ...);
 

@@ -1081,6 +1081,7 @@ void filter_mode(int kind, bool has_a, bool has_b, int spatial_only, int& mode, 
 }
 
 int plan_factors(int D, Plan& p) {
+  p = Plan{};  // every byte defined: const_upload compares the whole struct
   p.D = D;
   p.nf = 0;
   int x = D;
@@ -1128,7 +1129,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   const int kb_used = (mode == 2) ? 0 : kb;
   bool uniform = true;
   for (int d = 0; d < D && uniform; ++d) uniform = dop_host[d] == (double)d / (double)D;
-  Plan plan;
+  Plan plan{};
   if (uniform && (!plan_factors(D, plan) || (size_t)3 * D * sizeof(cplx) > 200 * 1024)) uniform = false;
   if (!uniform && (size_t)q * sizeof(cplx) > 200 * 1024)
     return set_err(ctx, KST_ERR_DIMENSION, "detect: q=%d too long for the direct-sum path", q);
@@ -1170,6 +1171,7 @@ int detect(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cplx* 
   key.insert(key.end(), dop_host, dop_host + D);
   key.insert(key.end(), (const double*)grid_host, (const double*)grid_host + 2 * (size_t)G * p);
   if (ctx->det_base != base || ctx->det_key != key) {
+    epoch_bump("detect tables", D);
     for (int e = 0; e < G * p; ++e) hstage[e] = cconj(grid_host[e]);
     double* hdop = (double*)(hstage + (size_t)G * p);
     for (int d = 0; d < D; ++d) hdop[d] = dop_host[d];
@@ -1287,7 +1289,7 @@ int spectra(kst_ctx* ctx, const cplx* x, int64_t rows, int q, const double* dop_
   if (rows == 0) return KST_OK;
   bool uniform = true;
   for (int d = 0; d < D && uniform; ++d) uniform = dop_host[d] == (double)d / (double)D;
-  Plan plan;
+  Plan plan{};
   if (uniform && (!plan_factors(D, plan) || (size_t)3 * D * sizeof(cplx) > 200 * 1024)) uniform = false;
   if (!uniform && (size_t)q * sizeof(cplx) > 200 * 1024)
     return set_err(ctx, KST_ERR_DIMENSION, "spectra: q=%d too long for the direct-sum path", q);
@@ -1328,6 +1330,7 @@ int filter_cube(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const c
   char* base = (char*)ws_get(ctx, WS_DET, sizeof(cplx) * (size_t)rows * std::max(kb_used, 1) + 256);
   if (!base) return set_err(ctx, KST_ERR_CUDA, "filter: workspace");
   ctx->det_base = nullptr;  // overwrites detect's resident grid / twiddles
+  epoch_bump("filter", 0);
   cplx* coef = (cplx*)base;
   int* flag = (int*)(coef + (size_t)rows * std::max(kb_used, 1));
   KST_CUDA(ctx, cudaMemsetAsync(flag, 0, sizeof(int), st));

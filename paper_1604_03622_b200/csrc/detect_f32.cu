@@ -662,7 +662,7 @@ bool pencil_ok(int R) {
 // powers, Cooley-Tukey a x b inside a factor above 32)
 struct CachedPlan {
   bool ok = false;
-  F32Plan plan;
+  F32Plan plan{};
   std::vector<uint16_t> u16;  // pos_in (D), pos_out (D), bases (nbase)
   std::vector<float2> w;      // per-stage W tables (nw)
   std::vector<float2> ctw;    // Cooley-Tukey twiddles
@@ -838,6 +838,7 @@ int detect_f32(kst_ctx* ctx, const cplx* cube, int64_t n, int p, int q, const cp
   double2* qh = (double2*)(ws + tab_bytes + b_ubf);
   float2* qf = (float2*)(qh + 4 * F32_MAXP);
   if (ctx->f32_base != (const void*)ws || ctx->f32_D != D) {  // tables resident per (buffer, D)
+    epoch_bump("f32 tables", D);
     char* hs = (char*)pinned_get(ctx, tab_bytes);
     if (!hs) return set_err(ctx, KST_ERR_CUDA, "detect_f32: pinned staging");
     memcpy(hs, cp.u16.data(), sizeof(uint16_t) * cp.u16.size());

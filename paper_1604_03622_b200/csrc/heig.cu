@@ -199,12 +199,21 @@ __global__ void gram_partial_kernel(const cplx* __restrict__ U, int ldu, int s1,
   }
 }
 
-// out[e] = sum_blk partial[blk][e], fixed order
+// out[e] = sum_blk partial[blk][e], fixed order (eight loads in flight, the
+// additions in block order)
 __global__ void reduce_partials_kernel(const cplx* __restrict__ partial, int nblk, int count,
                                        cplx* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
     cplx acc = cmk(0, 0);
-    for (int b = 0; b < nblk; ++b) acc = cadd(acc, partial[(size_t)b * count + e]);
+    int b = 0;
+    for (; b + 8 <= nblk; b += 8) {
+      cplx v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = partial[(size_t)(b + u) * count + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = cadd(acc, v[u]);
+    }
+    for (; b < nblk; ++b) acc = cadd(acc, partial[(size_t)b * count + e]);
     out[e] = acc;
   }
 }

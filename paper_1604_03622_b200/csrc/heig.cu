@@ -309,6 +309,9 @@ __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict
   for (int i = threadIdx.x; i < dyn_n; i += blockDim.x) dg[i] = B[(size_t)i * n + i].x;
   for (int e = threadIdx.x; e < n * s; e += blockDim.x) Z[e] = cmk(0, 0);
   __syncthreads();
+  // s rounds of a block argmax (ties -> lower i): thread -> warp (shuffles)
+  // -> warp 0 over the 32 warp winners (shuffles), two barriers per round
+  const int nw = (int)(blockDim.x >> 5);
   for (int k = 0; k < s; ++k) {
     double best = -INFINITY;
     int besti = n;
@@ -334,20 +337,21 @@ __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict
       bi[w] = besti;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double b0 = bv[0];
-      int i0 = bi[0];
-      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
-        if (bv[q] > b0 || (bv[q] == b0 && bi[q] < i0)) {
-          b0 = bv[q];
-          i0 = bi[q];
+    if (w == 0) {
+      double b0 = l < nw ? bv[l] : -INFINITY;
+      int i0 = l < nw ? bi[l] : n;
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, b0, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i0, o);
+        if (ob > b0 || (ob == b0 && oi < i0)) {
+          b0 = ob;
+          i0 = oi;
         }
-      if (i0 >= n) i0 = k;  // fewer candidates than s (cannot happen for n > 64)
-      picked[k] = i0;
+      }
+      if (l == 0) picked[k] = i0 >= n ? k : i0;  // fewer candidates than s (cannot happen for n > 64)
     }
     __syncthreads();
   }
-  __syncthreads();
   if (threadIdx.x < s) Z[(size_t)picked[threadIdx.x] * s + threadIdx.x] = cmk(1.0, 0.0);
 }
 

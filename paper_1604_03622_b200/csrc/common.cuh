@@ -299,7 +299,8 @@ struct TopEig {
   cplx* vectors = nullptr;     // dev (n, r) row-major
 };
 int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cplx* vectors,
-             cudaStream_t st, int* ok_dev = nullptr, const double** values_dev_out = nullptr);
+             cudaStream_t st, int* ok_dev = nullptr, const double** values_dev_out = nullptr,
+             const double* mdiag = nullptr /* Re diag(M), contiguous (optional) */);
 int small_heig(kst_ctx* ctx, const cplx* M, int n, double* values_dev, cplx* vectors_dev,
                cudaStream_t st);
 int truncate_from_pairs(kst_ctx* ctx, const double* values_host, const cplx* vectors, int n,

@@ -300,28 +300,38 @@ __global__ void random_block_kernel(cplx* Z, int n, int s, uint64_t seed) {
 // strided loads in flight together) when it fits (dyn_n > 0), and the s
 // selection rounds then read smem.
 __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict__ B, int n, int s,
-                                                          cplx* __restrict__ Z, int dyn_n) {
+                                                          cplx* __restrict__ Z, int dyn_n,
+                                                          const double* __restrict__ mdiag) {
   extern __shared__ double dg[];
   __shared__ int picked[32];
   __shared__ double bv[32];
   __shared__ int bi[32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < dyn_n; i += blockDim.x) dg[i] = B[(size_t)i * n + i].x;
-  for (int e = threadIdx.x; e < n * s; e += blockDim.x) Z[e] = cmk(0, 0);
-  __syncthreads();
+  for (int i = threadIdx.x; i < dyn_n; i += blockDim.x) dg[i] = mdiag ? mdiag[i] : B[(size_t)i * n + i].x;
+  __syncthreads();  // Z was zeroed by the caller (memset: the whole GPU, not one SM)
   // s rounds of a block argmax (ties -> lower i): thread -> warp (shuffles)
   // -> warp 0 over the 32 warp winners (shuffles), two barriers per round
   const int nw = (int)(blockDim.x >> 5);
   for (int k = 0; k < s; ++k) {
     double best = -INFINITY;
     int besti = n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      bool used = false;
-      for (int j = 0; j < k; ++j) used |= picked[j] == i;
-      const double v = dyn_n ? dg[i] : B[(size_t)i * n + i].x;
-      if (!used && (v > best || (v == best && i < besti))) {
-        best = v;
-        besti = i;
+    if (dyn_n) {  // picked entries are knocked out of the staged diagonal (finite values)
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = dg[i];
+        if (v > best || (v == best && i < besti)) {
+          best = v;
+          besti = i;
+        }
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        bool used = false;
+        for (int j = 0; j < k; ++j) used |= picked[j] == i;
+        const double v = B[(size_t)i * n + i].x;
+        if (!used && (v > best || (v == best && i < besti))) {
+          best = v;
+          besti = i;
+        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -348,7 +358,10 @@ __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict
           i0 = oi;
         }
       }
-      if (l == 0) picked[k] = i0 >= n ? k : i0;  // fewer candidates than s (cannot happen for n > 64)
+      if (l == 0) {
+        picked[k] = i0 >= n ? k : i0;  // fewer candidates than s (cannot happen for n > 64)
+        if (dyn_n && i0 < n) dg[i0] = -INFINITY;
+      }
     }
     __syncthreads();
   }
@@ -1004,7 +1017,7 @@ static int heig_top_cusolver(kst_ctx* ctx, const cplx* M, int n, int r, double* 
 // the host loop would have stopped after that round, 0 otherwise), values
 // left on the device (*values_dev_out); no stream synchronisation.
 int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cplx* vectors,
-             cudaStream_t st, int* ok_dev, const double** values_dev_out) {
+             cudaStream_t st, int* ok_dev, const double** values_dev_out, const double* mdiag) {
   if (r < 1 || r > n) return set_err(ctx, KST_ERR_DIMENSION, "heig_top: r=%d n=%d", r, n);
   if (ok_dev && (n <= kMaxN || r > 24))
     return set_err(ctx, KST_ERR_DIMENSION, "heig_top: no sync-free form for n=%d r=%d", n, r);
@@ -1079,7 +1092,8 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
     if (dyn_n > 6 * 1024)
       KST_CUDA(ctx, cudaFuncSetAttribute(unit_start_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(double) * dyn_n)));
-    unit_start_kernel<<<1, 1024, sizeof(double) * dyn_n, st>>>(M, n, s, Z, dyn_n);
+    KST_CUDA(ctx, cudaMemsetAsync(Z, 0, sizeof(cplx) * (size_t)n * s, st));
+    unit_start_kernel<<<1, 1024, sizeof(double) * dyn_n, st>>>(M, n, s, Z, dyn_n, mdiag);
   }
   KST_LAUNCH(ctx);
   // Warm-up without Rayleigh-Ritz (Ritz pairs of the start block are useless):

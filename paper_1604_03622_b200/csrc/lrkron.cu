@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(NT) init_kernel(const double* __restrict__ par
 template <int P>
 __global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, int q,
                                                    const IterState* __restrict__ st,
-                                                   cplx* __restrict__ b, double* __restrict__ part) {
+                                                   cplx* __restrict__ b, double* __restrict__ part,
+                                                   double* __restrict__ bdiag = nullptr) {
   __shared__ cplx ca[P * P];
   __shared__ double sh[32];
   for (int e = threadIdx.x; e < P * P; e += NT) ca[e] = st->Aconj[e];
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(NT) bstep_kernel(const cplx* __restrict__ S, i
     }
     acc = cmk(acc.x / na2, acc.y / na2);
     b[(int64_t)r * q + c] = acc;
+    if (bdiag && c == r) bdiag[r] = acc.x;  // Re diag(b), contiguous for the eigensolver's start block
     nb = cabs2(acc);
   }
   nb = block_sum<NT>(nb, sh);
@@ -723,7 +725,7 @@ int lrkron(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, double tol
   // the M-path records): a second ws_get on a grown slot would free the buffer
   // the b-step partials still point into.
   size_t part_bytes = std::max(sizeof(double) * stat_stride * p * nbx,
-                               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64);
+                               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * (nbb + 1) + 64);
   if (mpath) part_bytes = std::max(part_bytes, sizeof(double) * rec * nblk + 64);
   char* small = (char*)ws_get(ctx, WS_SMALL, sizeof(IterState) + 256);
   double* part = (double*)ws_get(ctx, WS_PART, part_bytes);
@@ -931,7 +933,7 @@ int lrkron_async(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, doub
   KST_DISPATCH_P(p, (rec = MDims<PP>::STRIDE));
   // the same slots and sizes as lrkron (WS_PART taken once for every use)
   size_t part_bytes = std::max(sizeof(double) * STAT_STRIDE * p * nbx,
-                               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * nbb + 64);
+                               sizeof(cplx) * (size_t)p * nvx * p + sizeof(double) * (size_t)q * (nbb + 1) + 64);
   part_bytes = std::max(part_bytes, sizeof(double) * rec * nblk + 64);
   char* small = (char*)ws_get(ctx, WS_SMALL, sizeof(IterState) + 256);
   double* part = (double*)ws_get(ctx, WS_PART, part_bytes);
@@ -972,9 +974,10 @@ int lrkron_async(kst_ctx* ctx, const cplx* S, int p, int q, int ra, int rb, doub
   // final b from the A that entered the last iteration (st->Aconj / st->na2)
   cplx* vpart = (cplx*)part;
   double* bpart = (double*)(vpart + (size_t)p * nvx * p);
-  KST_DISPATCH_P(p, (bstep_kernel<PP><<<dim3(nbb, q), NT, 0, st>>>(S, q, state, b, bpart)));
+  double* bdiag = bpart + (size_t)q * nbb;
+  KST_DISPATCH_P(p, (bstep_kernel<PP><<<dim3(nbb, q), NT, 0, st>>>(S, q, state, b, bpart, bdiag)));
   KST_LAUNCH(ctx);
-  KST_TRY(heig_top(ctx, b, q, rb, nullptr, tb_vectors, st, heig_ok, tb_vals_dev));
+  KST_TRY(heig_top(ctx, b, q, rb, nullptr, tb_vectors, st, heig_ok, tb_vals_dev, bdiag));
   *dres_out = dres;
   *diag_out = diag;
   return KST_OK;

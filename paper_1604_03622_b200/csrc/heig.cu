@@ -301,7 +301,8 @@ __global__ void random_block_kernel(cplx* Z, int n, int s, uint64_t seed) {
 // selection rounds then read smem.
 __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict__ B, int n, int s,
                                                           cplx* __restrict__ Z, int dyn_n,
-                                                          const double* __restrict__ mdiag) {
+                                                          const double* __restrict__ mdiag,
+                                                          int* __restrict__ picked_out) {
   extern __shared__ double dg[];
   __shared__ int picked[32];
   __shared__ double bv[32];
@@ -365,7 +366,22 @@ __global__ void __launch_bounds__(1024) unit_start_kernel(const cplx* __restrict
     }
     __syncthreads();
   }
-  if (threadIdx.x < s) Z[(size_t)picked[threadIdx.x] * s + threadIdx.x] = cmk(1.0, 0.0);
+  if (threadIdx.x < s) {
+    Z[(size_t)picked[threadIdx.x] * s + threadIdx.x] = cmk(1.0, 0.0);
+    picked_out[threadIdx.x] = picked[threadIdx.x];
+  }
+}
+
+// Y = B Z0 for the unit-vector start block: Y[i][c] = conj(B[p_c][i]) (row p_c
+// of the Hermitian B read contiguously), the value bz2_kernel forms as
+// conj(sum_k B[k][i] conj(Z0[k][c])) -- no pass over all of B
+__global__ void start_cols_kernel(const cplx* __restrict__ B, int n, int s, const int* __restrict__ picked,
+                                  cplx* __restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * s;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n), i = (int)(e % n);
+    Y[(size_t)i * s + c] = cconj(B[(size_t)picked[c] * n + i]);
+  }
 }
 
 // heig_top's Rayleigh-Ritz convergence test, on the device for both the
@@ -1093,13 +1109,15 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
       KST_CUDA(ctx, cudaFuncSetAttribute(unit_start_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(sizeof(double) * dyn_n)));
     KST_CUDA(ctx, cudaMemsetAsync(Z, 0, sizeof(cplx) * (size_t)n * s, st));
-    unit_start_kernel<<<1, 1024, sizeof(double) * dyn_n, st>>>(M, n, s, Z, dyn_n, mdiag);
+    int* picked = (int*)partial;  // scratch: consumed before k4_gram writes the partials
+    unit_start_kernel<<<1, 1024, sizeof(double) * dyn_n, st>>>(M, n, s, Z, dyn_n, mdiag, picked);
+    KST_LAUNCH(ctx);
+    start_cols_kernel<<<grid_for((int64_t)n * s), 256, 0, st>>>(M, n, s, picked, Y);  // Y = B Z0
   }
   KST_LAUNCH(ctx);
   // Warm-up without Rayleigh-Ritz (Ritz pairs of the start block are useless):
   // Z <- orth(B^4 Z0), two orthonormalisation passes (SVQB when the block is
   // ill-conditioned, Cholesky-QR once it is not).
-  KST_TRY(bz(ctx, M, n, Z, s, Y, st));
   KST_TRY(bz(ctx, M, n, Y, s, Y2, st));
   KST_TRY(bz(ctx, M, n, Y2, s, Y, st));
   KST_TRY(bz(ctx, M, n, Y, s, Y2, st));

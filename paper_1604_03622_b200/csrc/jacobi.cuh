@@ -196,6 +196,27 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
   const unsigned magic_n = 0xFFFFFFFFu / (unsigned)n + 1u;
   const unsigned magic_pn = 0xFFFFFFFFu / (unsigned)(npairs * n) + 1u;
   for (int sweep = 0; sweep < 40; ++sweep) {
+    if (sweep > 0) {
+      // would this sweep rotate at all? Every pair's test on the current A
+      // (a sweep that rotates nothing leaves A unchanged, so its per-round
+      // tests all see this A): the final, empty sweep -- n - 1 rounds of four
+      // barriers -- becomes one parallel check with the same thresholds
+      int rot = 0;
+      for (int e = tid; e < n * n; e += nt) {
+        const int a = (int)__umulhi((unsigned)e, magic_n), b = e - a * n;
+        if (a < b) {
+          const double app = j.A[a * j.ld + a].x, aqq = j.A[b * j.ld + b].x;
+          const cplx apq = j.A[a * j.ld + b];
+          const double r2 = apq.x * apq.x + apq.y * apq.y;
+          const double thr2 = fmax(4.84e-32 * fabs(app) * fabs(aqq), 1e-600 + 1e-30 * fro * fro);
+          rot |= r2 > thr2;
+        }
+      }
+      if (!__syncthreads_or(rot)) {
+        if (tid == 0) j.flag[1] = sweep;  // diagnostic: sweeps used
+        break;
+      }
+    }
     if (tid == 0) *j.flag = 0;
     __syncthreads();
     for (int round = 0; round < m - 1; ++round) {

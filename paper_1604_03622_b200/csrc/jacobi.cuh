@@ -290,22 +290,24 @@ __device__ inline void jac_sweeps(JacSmem& j, int n) {
         const int k = (int)__umulhi((unsigned)e, magic_n), col = e - k * n;
         const int p = j.pp[k], q = j.pq[k];
         if (q >= n || j.s[k] == 0.0) continue;
+        // the pair's own 2 x 2 block takes its exact post-rotation values
+        // (real diagonal, zero off-diagonal) in the same pass
+        if (col == p) {
+          j.A[p * j.ld + p] = cmk(j.scratch[2 * k], 0.0);
+          j.A[q * j.ld + p] = cmk(0.0, 0.0);
+          continue;
+        }
+        if (col == q) {
+          j.A[p * j.ld + q] = cmk(0.0, 0.0);
+          j.A[q * j.ld + q] = cmk(j.scratch[2 * k + 1], 0.0);
+          continue;
+        }
         const double c = j.c[k], s = j.s[k];
         const cplx epi = cmk(j.ec[k], j.es[k]);  // e^{i phi}
         const cplx xp = j.A[p * j.ld + col], xq = j.A[q * j.ld + col];
         const cplx wq = cmul(epi, xq);
         j.A[p * j.ld + col] = cmk(c * xp.x - s * wq.x, c * xp.y - s * wq.y);
         j.A[q * j.ld + col] = cmk(s * xp.x + c * wq.x, s * xp.y + c * wq.y);
-      }
-      __syncthreads();
-      if (tid < npairs) {
-        const int p = j.pp[tid], q = j.pq[tid];
-        if (q < n && j.s[tid] != 0.0) {
-          j.A[p * j.ld + p] = cmk(j.scratch[2 * tid], 0.0);
-          j.A[q * j.ld + q] = cmk(j.scratch[2 * tid + 1], 0.0);
-          j.A[p * j.ld + q] = cmk(0.0, 0.0);
-          j.A[q * j.ld + p] = cmk(0.0, 0.0);
-        }
       }
       __syncthreads();
     }

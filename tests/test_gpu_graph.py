@@ -89,3 +89,20 @@ def test_pipeline_async_rejects_ineligible_shapes():
     fg = kst.FrameGraph(buf, 1, 3)
     with pytest.raises(kst.DimensionError):
         fg.replay()
+
+
+@pytest.mark.parametrize("kind,groups", [("classical", 1), ("kron", 2), ("classical", 2)])
+def test_graph_other_kinds_and_groups(kind, groups):
+    """Replays equal the direct call for the other filter kinds and for
+    multi-group (stacked) detection maps."""
+    p, q, n = 3, 130, 60
+    D, G = q, 16
+    dop, grid = kst.make_doppler_grid(D), kst.make_spatial_grid(p, G)
+    cube = frames(p, q, n, 1, seed=21)[0]
+    buf = torch.from_numpy(cube).cuda()
+    ref, rsum = kst.process_frame_device(buf, 1, 3, dopplers=dop, spatial_grid=grid, kind=kind,
+                                         groups=groups)
+    fg = kst.FrameGraph(buf, 1, 3, dopplers=dop, spatial_grid=grid, kind=kind, groups=groups)
+    fg.replay()
+    vals, summ = fg.result()
+    assert torch.equal(vals, ref) and np.array_equal(summ[:5], rsum[:5])

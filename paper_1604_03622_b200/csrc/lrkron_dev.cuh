@@ -40,13 +40,17 @@ __device__ __noinline__ int spatial_update(const cplx* V, double nb2, int P, int
                               char* sm, cplx* Anew, double* lam, int* bad_s, double* eta_out,
                               int* conv_out) {
   const int tid = threadIdx.x;
-  // eig_truncate(V / nb2, ra): Hermitian check first (src/linalg.py:68-79)
+  // eig_truncate(V / nb2, ra): Hermitian check first (src/linalg.py:68-79);
+  // the P^2 quotients by all threads, the sums in order by one
+  __shared__ cplx vq[kMaxP * kMaxP];
+  for (int e = tid; e < P * P; e += NT) vq[e] = cmk(V[e].x / nb2, V[e].y / nb2);
+  __syncthreads();
   if (tid == 0) {
     double f = 0.0, a = 0.0;
     for (int r = 0; r < P; ++r)
       for (int c = 0; c < P; ++c) {
-        const cplx x = cmk(V[r * P + c].x / nb2, V[r * P + c].y / nb2);
-        const cplx y = cmk(V[c * P + r].x / nb2, V[c * P + r].y / nb2);
+        const cplx x = vq[r * P + c];
+        const cplx y = vq[c * P + r];
         f += cabs2(x);
         a += cabs2(cmk(x.x - y.x, x.y + y.y));
         if (!isfinite(x.x) || !isfinite(x.y)) a = INFINITY;
@@ -154,15 +158,18 @@ __device__ void m_iterations(const double* red, int q, int ra, double tol, int m
     M[u * U + v] = m;
     M[v * U + u] = cconj(m);
   }
-  if (tid == 0) {
+  {  // A0 = block sums / q^2: the quotients by all threads, |A0|^2 in order by one
     const double qq = (double)q * (double)q;
-    double na2 = 0.0;
-    for (int e = 0; e < U; ++e) {
+    for (int e = tid; e < U; e += NT) {
       const cplx a = cmk(red[4 + 2 * e] / qq, red[5 + 2 * e] / qq);
       st->A[e] = a;
       st->Aconj[e] = cconj(a);
-      na2 += cabs2(a);
     }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double na2 = 0.0;
+    for (int e = 0; e < U; ++e) na2 += cabs2(st->A[e]);
     st->fro2 = red[0];
     st->fro = sqrt(red[0]);
     st->na2 = na2;
@@ -202,10 +209,10 @@ __device__ void m_iterations(const double* red, int q, int ra, double tol, int m
         double q2 = 0.0;
         for (int u = 0; u < U; ++u) q2 += st->A[u].x * Ma[u].x + st->A[u].y * Ma[u].y;
         scal[1] = q2 / (na2 * na2);
-        for (int u = 0; u < U; ++u) V[u] = cmk(Ma[u].x / na2, Ma[u].y / na2);
         // the A that produces this iteration's b (kept for the final b-step)
         scal[2] = na2;
       }
+      for (int u = tid; u < U; u += NT) V[u] = cmk(Ma[u].x / na2, Ma[u].y / na2);
       __syncthreads();
       const double nb2 = scal[1];
       ++iters;

@@ -1168,6 +1168,17 @@ int heig_top(kst_ctx* ctx, const cplx* M, int n, int r, double* values_host, cpl
         if (jx != k) gap = std::min(gap, std::fabs(th[k] - th[jx]));
       all_ok = all_ok && (res <= 1e-12 * tmax || (res <= 1e-9 * tmax && res <= 1e-8 * gap));
     }
+    {
+      static const bool dbg = getenv("KST_HEIG_DEBUG") != nullptr;  // convergence margins
+      if (dbg)
+        for (int k = 0; k < r; ++k) {
+          double gap = 1e300;
+          for (int jx = 0; jx < s; ++jx)
+            if (jx != k) gap = std::min(gap, std::fabs(th[k] - th[jx]));
+          fprintf(stderr, "[heig_top] round %d pair %d: res/tmax %.3e (1e-12), res/gap %.3e (1e-8)\n",
+                  it, k, std::sqrt(hred[k]) / tmax, std::sqrt(hred[k]) / gap);
+        }
+    }
     if (kept == 0) break;  // B^2 Z vanished: leave it to the dense solver
     if (tmax == 0.0 || all_ok) {
       converged = true;

@@ -152,3 +152,13 @@ def test_window_partition_covers_every_bin_once():
             seen.extend(range(lo, hi))
             assert all(window_start(m, n_w, n_bins) == s for m in range(lo, hi))
         assert seen == list(range(n_bins))
+
+
+def test_frame_graph_rejects_host_cubes():
+    """FrameGraph captures a device buffer: host tensors and wrong ranks are
+    refused before anything touches the library (no CPU fallback)."""
+    import torch
+    with pytest.raises(kst.DimensionError):
+        kst.FrameGraph(torch.zeros((4, 3, 96), dtype=torch.complex128))
+    with pytest.raises(kst.DimensionError):
+        kst.FrameGraph(torch.zeros((4, 96), dtype=torch.complex128))
